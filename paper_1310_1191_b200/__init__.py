@@ -1,0 +1,366 @@
+"""B200-native prismatic element integration (arXiv 1310.1191 hot path).
+
+Python mirror of the reference's integration interface (prismint,
+/root/reference/proj), driving the sm_100a kernels through the C ABI in
+``include/prism_b200.h`` (library ``libprism_b200.so``, built in-tree).
+
+Reference name            -> here
+  prism_quadrature(p)        prism_quadrature(p)            (reference_element.cpp:175)
+  tabulate_shapes(p, rule)   tabulate_shapes(p, points)     (reference_element.cpp:272)
+  generate_box_mesh(...)     generate_box_mesh(...)         (geometry.cpp:134)
+  integrate_generic(...)     Integrator.integrate_device / integrate_host (batched)
+  run_batch(...)             run_batch(...)                 (kernels.cpp:485)
+  prismint::Error & co.      Error, ConfigError, ... InvertedElementError
+
+There is no CPU fallback: importing works without a GPU (for the host-side
+helpers), but every integration call requires the CUDA library and a device
+and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+__all__ = [
+    "Error", "ConfigError", "DomainError", "UnsupportedDegreeError", "InvertedElementError",
+    "CapacityError", "SharedMemoryError", "ContractViolation", "IoError", "CudaError",
+    "LAPLACE", "UNIFORM", "PER_ELEMENT", "OUT_CANONICAL", "OUT_SOA",
+    "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
+    "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
+    "generate_box_mesh", "generate_cdr_coefficients", "laplace_tensor",
+    "Integrator", "run_batch", "flops_dense_per_element", "bytes_per_element", "library",
+]
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libprism_b200.so"
+
+LAPLACE, UNIFORM, PER_ELEMENT = 0, 1, 2
+OUT_CANONICAL, OUT_SOA = 0, 1
+VARIANT_AUTO, VARIANT_DENSE, VARIANT_SUMFACT = 0, 1, 2
+
+
+# ---- errors: prismint::errc (errors.hpp:10-19) plus CUDA ----
+class Error(RuntimeError):
+    code = "unknown"
+
+
+class ConfigError(Error):
+    code = "config"
+
+
+class DomainError(Error):
+    code = "domain"
+
+
+class UnsupportedDegreeError(Error):
+    code = "unsupported_degree"
+
+
+class InvertedElementError(Error):
+    """Carries the global element id, det and reference point (errors.hpp:43-54)."""
+    code = "inverted_element"
+
+    def __init__(self, message, element=-1, det=0.0, xi=(0.0, 0.0, 0.0)):
+        super().__init__(message)
+        self.element = element
+        self.det = det
+        self.xi = tuple(xi)
+
+
+class CapacityError(Error):
+    code = "capacity"
+
+
+class SharedMemoryError(Error):
+    code = "shared_memory_exhausted"
+
+
+class ContractViolation(Error):
+    code = "contract_violation"
+
+
+class IoError(Error):
+    code = "io"
+
+
+class CudaError(Error):
+    code = "cuda"
+
+
+_ERRORS = {1: ConfigError, 2: DomainError, 3: UnsupportedDegreeError, 4: InvertedElementError,
+           5: CapacityError, 6: SharedMemoryError, 7: ContractViolation, 8: IoError, 9: CudaError}
+
+
+class _ErrInfo(C.Structure):
+    _fields_ = [("element", C.c_int64), ("det", C.c_double), ("xi", C.c_double * 3),
+                ("cuda_error", C.c_int), ("message", C.c_char * 256)]
+
+
+_dp = C.POINTER(C.c_double)
+_lib = None
+
+
+def library():
+    """Loads libprism_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} not built: run `python __graft_entry__.py` build() or "
+                          f"`make -C paper_1310_1191_b200`")
+    L = C.CDLL(str(LIB_PATH))
+    E = C.POINTER(_ErrInfo)
+    vp = C.c_void_p
+    L.pi_shape_count.argtypes = [C.c_int]
+    L.pi_quadrature_point_count.argtypes = [C.c_int]
+    L.pi_prism_quadrature.argtypes = [C.c_int, _dp, _dp, E]
+    L.pi_tabulate_shapes.argtypes = [C.c_int, _dp, C.c_int, _dp, E]
+    L.pi_generate_box_mesh.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int64,
+                                       C.c_int64, C.c_int, C.c_int64, C.c_int, _dp, E]
+    L.pi_generate_cdr_coefficients.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int64, _dp, E]
+    L.pi_context_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp,
+                                    C.POINTER(vp), E]
+    L.pi_context_destroy.argtypes = [vp]
+    L.pi_context_set_variant.argtypes = [vp, C.c_int, E]
+    L.pi_context_variant.argtypes = [vp, C.c_int]
+    L.pi_context_stream.argtypes = [vp]
+    L.pi_context_stream.restype = vp
+    L.pi_integrate.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, C.c_int,
+                               C.c_int64, vp, E]
+    L.pi_load_vectors.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_double, vp, vp, E]
+    L.pi_check.argtypes = [vp, E]
+    L.pi_integrate_host.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int, vp, vp, C.c_int64, E]
+    L.pi_flops_dense_per_element.argtypes = [C.c_int, C.c_int, C.c_int]
+    L.pi_flops_dense_per_element.restype = C.c_double
+    L.pi_flops_executed_per_element.argtypes = [vp, C.c_int]
+    L.pi_flops_executed_per_element.restype = C.c_double
+    L.pi_bytes_per_element.argtypes = [C.c_int, C.c_int, C.c_int]
+    L.pi_bytes_per_element.restype = C.c_double
+    L.pi_status_name.restype = C.c_char_p
+    L.pi_version.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def _raise(status, err: _ErrInfo):
+    if status == 0:
+        return
+    cls = _ERRORS.get(status, Error)
+    msg = err.message.decode(errors="replace")
+    if cls is InvertedElementError:
+        raise InvertedElementError(msg, err.element, err.det, tuple(err.xi))
+    raise cls(msg)
+
+
+def _ptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def _addr(x):
+    """Raw address of a numpy array or torch tensor (device or host)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+# ---- per-p constants ----
+def shape_count(p: int) -> int:
+    n = library().pi_shape_count(p)
+    if n < 0:
+        raise DomainError(f"approximation order p={p} outside supported range [1, 7]")
+    return n
+
+
+def quadrature_point_count(p: int) -> int:
+    n = library().pi_quadrature_point_count(p)
+    if n < 0:
+        raise DomainError(f"approximation order p={p} outside supported range [1, 7]")
+    return n
+
+
+def prism_quadrature(p: int):
+    """(points [n_q][3], weights [n_q]) -- reference_element.cpp:175-193."""
+    nq = quadrature_point_count(p)
+    pts = np.zeros((nq, 3))
+    w = np.zeros(nq)
+    err = _ErrInfo()
+    _raise(library().pi_prism_quadrature(p, _ptr(pts), _ptr(w), C.byref(err)), err)
+    return pts, w
+
+
+def tabulate_shapes(p: int, points=None):
+    """[n_q][4][n_shape] -- reference_element.cpp:272-286."""
+    if points is None:
+        points, _ = prism_quadrature(p)
+    points = np.ascontiguousarray(points, dtype=np.float64)
+    out = np.zeros((len(points), 4, shape_count(p)))
+    err = _ErrInfo()
+    _raise(library().pi_tabulate_shapes(p, _ptr(points), len(points), _ptr(out), C.byref(err)), err)
+    return out
+
+
+def generate_box_mesh(nx, ny, nz, distortion, seed=0x5072697342657631, first=0, count=None, soa=False,
+                      ld=None, validate=False, out=None):
+    """Seeded box mesh (geometry.cpp:134-201).  AoS [count][6][3] or SoA [18][ld]."""
+    total = 2 * nx * ny * nz
+    count = total - first if count is None else count
+    if soa:
+        ld = count if ld is None else ld
+        out = np.zeros((18, ld)) if out is None else out
+    else:
+        out = np.zeros((count, 6, 3)) if out is None else out
+    err = _ErrInfo()
+    _raise(library().pi_generate_box_mesh(nx, ny, nz, distortion, seed, first, count, int(soa), ld or 0,
+                                          int(validate), _ptr(out), C.byref(err)), err)
+    return out
+
+
+def generate_cdr_coefficients(seed, first, count, soa=False, ld=None):
+    """Seeded convection-diffusion-reaction tensors, AoS [count][16] or SoA [16][ld]."""
+    if soa:
+        ld = count if ld is None else ld
+        out = np.zeros((16, ld))
+    else:
+        out = np.zeros((count, 16))
+    err = _ErrInfo()
+    _raise(library().pi_generate_cdr_coefficients(seed, first, count, int(soa), ld or 0, _ptr(out),
+                                                  C.byref(err)), err)
+    return out
+
+
+def laplace_tensor():
+    c = np.zeros((1, 1, 4, 4))
+    for d in range(1, 4):
+        c[0, 0, d, d] = 1.0
+    return c
+
+
+def flops_dense_per_element(p, coeff_mode=LAPLACE, n_eq=1):
+    return library().pi_flops_dense_per_element(p, n_eq, coeff_mode)
+
+
+def bytes_per_element(p, coeff_mode=LAPLACE, n_eq=1):
+    return library().pi_bytes_per_element(p, n_eq, coeff_mode)
+
+
+class Integrator:
+    """One context: device + p (+ the rule / shape table, the reference's own if given)."""
+
+    def __init__(self, p, device=0, n_eq=1, points=None, weights=None, shape_table=None, variant=VARIANT_AUTO):
+        L = library()
+        self.p = p
+        self.n_eq = n_eq
+        self.n_shape = shape_count(p)
+        self.n_q = quadrature_point_count(p)
+        self.dim = n_eq * self.n_shape
+        self._keep = []
+        args = [None, None, None]
+        if points is not None:
+            arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (points, weights, shape_table)]
+            self._keep = arrs
+            args = [_ptr(a) for a in arrs]
+        h = C.c_void_p()
+        err = _ErrInfo()
+        _raise(L.pi_context_create(device, p, n_eq, self.n_q, self.n_shape, *args, C.byref(h), C.byref(err)), err)
+        self._h = h
+        if variant != VARIANT_AUTO:
+            self.set_variant(variant)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            library().pi_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_variant(self, variant):
+        err = _ErrInfo()
+        _raise(library().pi_context_set_variant(self._h, variant, C.byref(err)), err)
+
+    def variant(self, coeff_mode=LAPLACE):
+        return library().pi_context_variant(self._h, coeff_mode)
+
+    @property
+    def stream(self):
+        return library().pi_context_stream(self._h)
+
+    def flops_executed_per_element(self, coeff_mode=LAPLACE):
+        return library().pi_flops_executed_per_element(self._h, coeff_mode)
+
+    # -- device buffers (torch tensors or raw addresses); asynchronous --
+    def integrate_device(self, n_elem, geom, out, coeff_mode=LAPLACE, coeff=None, element_id_base=0,
+                         geom_ld=None, coeff_ld=None, out_layout=OUT_CANONICAL, ld_out=0, stream=None):
+        """pi_integrate on device memory.  geom: SoA [18][geom_ld]; out: device buffer."""
+        err = _ErrInfo()
+        cbuf = None
+        if coeff_mode == UNIFORM:
+            cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
+            caddr = cbuf.ctypes.data
+        else:
+            caddr = _addr(coeff) if coeff_mode == PER_ELEMENT else None
+        if geom_ld is None:
+            geom_ld = geom.shape[1] if hasattr(geom, "shape") else n_elem
+        if coeff_ld is None and coeff_mode == PER_ELEMENT:
+            coeff_ld = coeff.shape[1] if hasattr(coeff, "shape") else n_elem
+        st = library().pi_integrate(self._h, n_elem, element_id_base, _addr(geom) if not isinstance(geom, int) else geom,
+                                    geom_ld, coeff_mode, caddr, coeff_ld or 0,
+                                    _addr(out) if not isinstance(out, int) else out, out_layout, ld_out,
+                                    stream, C.byref(err))
+        _raise(st, err)
+
+    def load_vectors_device(self, n_elem, geom, out, f=None, f_const=1.0, element_id_base=0, geom_ld=None,
+                            stream=None):
+        err = _ErrInfo()
+        if geom_ld is None:
+            geom_ld = geom.shape[1] if hasattr(geom, "shape") else n_elem
+        st = library().pi_load_vectors(self._h, n_elem, element_id_base, _addr(geom), geom_ld, _addr(f),
+                                       float(f_const), _addr(out), stream, C.byref(err))
+        _raise(st, err)
+
+    def check(self):
+        """Synchronises and raises InvertedElementError / CudaError (pi_check)."""
+        err = _ErrInfo()
+        _raise(library().pi_check(self._h, C.byref(err)), err)
+
+    # -- host buffers: the run_batch-style drop-in --
+    def integrate_host(self, geoms, coeff_mode=LAPLACE, coeff=None, element_id_base=0, out=None, chunk_elems=0):
+        """geoms: host [n][6][3]; returns host [n][dim][dim] (canonical)."""
+        geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
+        n = len(geoms)
+        if out is None:
+            out = np.empty((n, self.dim, self.dim))
+        cbuf = None
+        if coeff_mode == UNIFORM:
+            cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
+        elif coeff_mode == PER_ELEMENT:
+            cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(n, -1)
+        err = _ErrInfo()
+        st = library().pi_integrate_host(self._h, n, element_id_base, _addr(geoms), coeff_mode, _addr(cbuf),
+                                         _addr(out), chunk_elems, C.byref(err))
+        _raise(st, err)
+        return out
+
+
+def run_batch(p, mesh, coeff_mode=LAPLACE, coeff=None, device=0, **kw):
+    """run_batch (kernels.cpp:485-514) semantics: matrices in mesh order."""
+    if len(mesh) == 0:
+        raise ConfigError("run_batch: empty mesh")
+    with Integrator(p, device=device, **kw) as it:
+        return it.integrate_host(mesh, coeff_mode, coeff)

@@ -1,0 +1,116 @@
+// Device helpers shared by the integration kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/prism_b200.h"
+
+namespace pib {
+
+// Per-launch arguments common to every strategy.
+struct LaunchArgs {
+  int64_t n_elem;
+  int64_t element_id_base;
+  const double* geom;   // SoA [18][geom_ld]
+  int64_t geom_ld;
+  const double* coeff;  // PER_ELEMENT: SoA [16][coeff_ld]; else nullptr
+  int64_t coeff_ld;
+  double cu[16];        // UNIFORM coefficient tensor (GENERAL kernels)
+  double* out;
+  int out_layout;
+  int64_t ld_out;
+  unsigned long long* bad;  // min offending global element id (atomicMin)
+};
+
+// Jacobian of the multilinear prism map at xi (geometry.cpp:32-58) for the
+// SoA/smem vertex array x[v*3+i], its determinant and the cofactor inverse
+// inv[k][i] = dxi_k/dx_i (geometry.cpp:60-83).  Returns det.
+__device__ __forceinline__ double prism_jacobian(const double* __restrict__ x, double xi1, double xi2,
+                                                 double xi3, double inv[3][3]) {
+  const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
+  const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
+  double j[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    j[i][0] = zm * (x[3 + i] - x[0 + i]) + zp * (x[12 + i] - x[9 + i]);
+    j[i][1] = zm * (x[6 + i] - x[0 + i]) + zp * (x[15 + i] - x[9 + i]);
+    j[i][2] = l0 * (x[9 + i] - x[0 + i]) + l1 * (x[12 + i] - x[3 + i]) + l2 * (x[15 + i] - x[6 + i]);
+  }
+  const double c00 = j[1][1] * j[2][2] - j[1][2] * j[2][1];
+  const double c01 = j[1][2] * j[2][0] - j[1][0] * j[2][2];
+  const double c02 = j[1][0] * j[2][1] - j[1][1] * j[2][0];
+  const double det = j[0][0] * c00 + j[0][1] * c01 + j[0][2] * c02;
+  const double id = 1.0 / det;
+  inv[0][0] = c00 * id;
+  inv[0][1] = (j[0][2] * j[2][1] - j[0][1] * j[2][2]) * id;
+  inv[0][2] = (j[0][1] * j[1][2] - j[0][2] * j[1][1]) * id;
+  inv[1][0] = c01 * id;
+  inv[1][1] = (j[0][0] * j[2][2] - j[0][2] * j[2][0]) * id;
+  inv[1][2] = (j[0][2] * j[1][0] - j[0][0] * j[1][2]) * id;
+  inv[2][0] = c02 * id;
+  inv[2][1] = (j[0][1] * j[2][0] - j[0][0] * j[2][1]) * id;
+  inv[2][2] = (j[0][0] * j[1][1] - j[0][1] * j[1][0]) * id;
+  return det;
+}
+
+// Reference-coordinate coefficient block M = T (dw C) T^T with
+// T = diag(1, inv): then K_ij = sum_q sum_kl phi_k(i,q) M_kl(q) phi_l(j,q),
+// an exact re-association of integrate_generic's
+// sum_q sum_ab (dw c_ab) psi_a(i) psi_b(j) (integrate_ref.cpp:79-88), with
+// psi from physical_derivatives (geometry.cpp:85-102).  M is 4x4 row-major.
+template <bool GENERAL>
+__device__ __forceinline__ void coefficient_block(const double inv[3][3], double dw, const double* c,
+                                                  double M[16]) {
+  if (!GENERAL) {
+    // Laplace: c[d][d] = 1 (d = 1..3): M_kl = dw * sum_d inv[k][d] inv[l][d].
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int l = k; l < 3; ++l) {
+        const double v = dw * (inv[k][0] * inv[l][0] + inv[k][1] * inv[l][1] + inv[k][2] * inv[l][2]);
+        M[(k + 1) * 4 + (l + 1)] = v;
+        M[(l + 1) * 4 + (k + 1)] = v;
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      M[k] = 0.0;
+      M[k * 4] = 0.0;
+    }
+  } else {
+    double cd[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) cd[i] = dw * c[i];
+    // W = C' T^T: W[a][l] = sum_b C'[a][b] T[l][b]
+    double W[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      W[a][0] = cd[a * 4 + 0];
+#pragma unroll
+      for (int l = 1; l < 4; ++l)
+        W[a][l] = cd[a * 4 + 1] * inv[l - 1][0] + cd[a * 4 + 2] * inv[l - 1][1] + cd[a * 4 + 3] * inv[l - 1][2];
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      M[0 * 4 + l] = W[0][l];
+#pragma unroll
+      for (int k = 1; k < 4; ++k)
+        M[k * 4 + l] = inv[k - 1][0] * W[1][l] + inv[k - 1][1] * W[2][l] + inv[k - 1][2] * W[3][l];
+    }
+  }
+}
+
+__device__ __forceinline__ void flag_inverted(unsigned long long* bad, int64_t gid) {
+  atomicMin(bad, static_cast<unsigned long long>(gid));
+}
+
+// D = A(8x4) * B(4x8) + D, FP64 tensor core (SASS DMMA.8x8x4).
+// Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// d0,d1 = D[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+}  // namespace pib

@@ -1,0 +1,144 @@
+// Thread-per-element dense integration (p = 1) and the load-vector kernel.
+//
+// At p = 1 the element matrix is 6x6 = 36 doubles, so one thread keeps all of
+// K in registers and walks the 6 rule points itself (the paper's
+// "one element per thread" organisation for the lowest order).  The shape
+// table (6 x 4 x 6 doubles) is read from shared memory as warp-wide
+// broadcasts; geometry and coefficients arrive as coalesced SoA loads; K
+// leaves through a shared-memory transpose so the canonical per-element
+// layout is written with contiguous 16-byte stores.
+#pragma once
+
+#include "kernels_common.cuh"
+
+namespace pib {
+
+struct DenseTables {
+  const double* phi;  // [NQ][4][NSH] (tabulate_shapes order)
+  const double* pts;  // [NQ][3]
+  const double* w;    // [NQ]
+};
+
+constexpr int kP1Threads = 128;
+
+template <bool GENERAL>
+__global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, DenseTables tab) {
+  constexpr int NQ = 6, NSH = 6, KK = NSH * NSH;
+  __shared__ double sPhi[NQ * 4 * NSH];
+  __shared__ double sPts[NQ * 3];
+  __shared__ double sW[NQ];
+  __shared__ __align__(16) double sOut[kP1Threads * KK];  // 36 KB staging
+
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NQ * 4 * NSH; i += kP1Threads) sPhi[i] = tab.phi[i];
+  if (tid < NQ * 3) sPts[tid] = tab.pts[tid];
+  if (tid < NQ) sW[tid] = tab.w[tid];
+  __syncthreads();
+
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * kP1Threads + tid;
+  const bool live = e < args.n_elem;
+  const int64_t ec = live ? e : args.n_elem - 1;
+  double x[18];
+#pragma unroll
+  for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+  double cf[16];
+  if (GENERAL) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) cf[c] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
+  }
+
+  double K[KK];
+#pragma unroll
+  for (int i = 0; i < KK; ++i) K[i] = 0.0;
+  bool inverted = false;
+
+#pragma unroll 1
+  for (int q = 0; q < NQ; ++q) {
+    double inv[3][3];
+    const double det = prism_jacobian(x, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], inv);
+    inverted |= !(det > 0.0);
+    double M[16];
+    coefficient_block<GENERAL>(inv, det * sW[q], cf, M);
+    const double* ph = sPhi + q * 4 * NSH;
+    constexpr int K0 = GENERAL ? 0 : 1;  // Laplace has no value row
+    // G_l(i) = sum_k phi_k(i) M_kl ; K_ij += sum_l G_l(i) phi_l(j)
+#pragma unroll
+    for (int i = 0; i < NSH; ++i) {
+      double g[4];
+#pragma unroll
+      for (int l = K0; l < 4; ++l) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = K0; k < 4; ++k) s += ph[k * NSH + i] * M[k * 4 + l];
+        g[l] = s;
+      }
+#pragma unroll
+      for (int j = GENERAL ? 0 : i; j < NSH; ++j) {
+        double s = K[i * NSH + j];
+#pragma unroll
+        for (int l = K0; l < 4; ++l) s += g[l] * ph[l * NSH + j];
+        K[i * NSH + j] = s;
+      }
+    }
+  }
+  if (!GENERAL) {  // Laplace: mirror the strict upper triangle
+#pragma unroll
+    for (int i = 0; i < NSH; ++i)
+#pragma unroll
+      for (int j = 0; j < i; ++j) K[i * NSH + j] = K[j * NSH + i];
+  }
+  if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
+
+  if (args.out_layout == PI_OUT_SOA) {
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < KK; ++i) args.out[i * args.ld_out + e] = K[i];
+    }
+    return;
+  }
+  // Canonical: stage [thread][36] in smem (odd stride in 16B units avoids
+  // bank conflicts: 36 doubles = 18 x 16 B), then write the CTA's contiguous
+  // block of 128 * 288 B with coalesced 16-byte stores.
+  double2* so2 = reinterpret_cast<double2*>(sOut);
+#pragma unroll
+  for (int i = 0; i < KK / 2; ++i) so2[tid * (KK / 2) + i] = make_double2(K[2 * i], K[2 * i + 1]);
+  __syncthreads();
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * kP1Threads;
+  const int64_t n_here = min(static_cast<int64_t>(kP1Threads), args.n_elem - first);
+  double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
+  const int total2 = static_cast<int>(n_here) * (KK / 2);
+  for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
+}
+
+// Load vectors: F_i = sum_q det_q w_q f phi_i(q) (value row).  One warp per
+// element: lanes split the shape functions; det*w per point is computed once
+// per element into shared memory.
+constexpr int kLoadWarps = 4;
+__global__ void __launch_bounds__(32 * kLoadWarps)
+    load_vector_kernel(LaunchArgs args, DenseTables tab, int nq, int nsh, const double* f, double f_const) {
+  extern __shared__ double sdw[];  // [kLoadWarps][nq]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * kLoadWarps + warp;
+  if (e >= args.n_elem) return;
+  double x[18];
+#pragma unroll
+  for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e];
+  const double fe = f ? f[e] : f_const;
+  double* dw = sdw + warp * nq;
+  bool inverted = false;
+  for (int q = lane; q < nq; q += 32) {
+    double inv[3][3];
+    const double det = prism_jacobian(x, tab.pts[3 * q], tab.pts[3 * q + 1], tab.pts[3 * q + 2], inv);
+    inverted |= !(det > 0.0);
+    dw[q] = det * tab.w[q] * fe;
+  }
+  if (__any_sync(0xffffffffu, inverted) && lane == 0) flag_inverted(args.bad, args.element_id_base + e);
+  __syncwarp();
+  for (int i = lane; i < nsh; i += 32) {
+    double s = 0.0;
+    for (int q = 0; q < nq; ++q) s += dw[q] * tab.phi[static_cast<int64_t>(q) * 4 * nsh + i];
+    args.out[e * nsh + i] = s;
+  }
+}
+
+}  // namespace pib

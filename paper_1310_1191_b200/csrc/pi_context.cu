@@ -1,0 +1,566 @@
+// C-ABI implementation: contexts, per-p table upload, strategy dispatch,
+// error reporting and the host-buffer streaming path.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels_dense.cuh"
+#include "kernels_sumfact.cuh"
+#include "pi_internal.hpp"
+
+using namespace pib;
+
+struct CallRecord {
+  const double* geom;
+  int64_t ld, base, n;
+};
+
+struct pi_context {
+  int device = 0, p = 0, n_eq = 1, n_q = 0, n_shape = 0;
+  int variant = PI_VARIANT_AUTO;
+  cudaStream_t stream = nullptr;
+  std::vector<double> h_pts, h_w, h_phi;
+  double *d_phi = nullptr, *d_pts = nullptr, *d_w = nullptr;
+  double *d_xfrag = nullptr, *d_yline = nullptr, *d_tri = nullptr;
+  bool tensor_ok = false;
+  unsigned long long* d_bad = nullptr;
+  std::vector<CallRecord> calls;
+  // host streaming path
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  double* hbuf = nullptr;
+  size_t hbuf_bytes = 0;
+};
+
+namespace {
+
+pi_status cuda_fail(pi_error_info* err, cudaError_t e, const char* what) {
+  if (err) err->cuda_error = static_cast<int>(e);
+  return set_error(err, PI_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define PI_CUDA(call, what)                                   \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(err, e_, what);   \
+  } while (0)
+
+// Structure-of-arrays transpose for the host path: AoS [n][w] -> SoA [w][ld].
+__global__ void aos_to_soa_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t n, int w,
+                                  int64_t ld) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * w) return;
+  const int64_t e = i / w;
+  const int c = static_cast<int>(i % w);
+  out[c * ld + e] = in[i];
+}
+
+template <int P>
+struct SumFactHost {
+  using C = SumFactConfig<P>;
+  static void set_attrs() {
+    cudaFuncSetAttribute(sumfact_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::SMEM_BYTES));
+    cudaFuncSetAttribute(sumfact_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::SMEM_BYTES));
+  }
+  static void launch(const LaunchArgs& a, const SumFactTables& t, bool general, cudaStream_t s) {
+    const int64_t groups = (a.n_elem + C::EPC - 1) / C::EPC;
+    const dim3 grid(static_cast<unsigned>(groups * C::NAG));
+    if (general)
+      sumfact_kernel<P, true><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+    else
+      sumfact_kernel<P, false><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+  }
+  // Builds the X fragment table, Y table and rule coordinates from the
+  // caller's rule and shape table; false if the table is not the tensor
+  // product the kernel factorises.
+  static bool build(pi_context* ctx, std::vector<double>& xfrag, std::vector<double>& yline,
+                    std::vector<double>& tri) {
+    constexpr int NS = C::NS, NZ = C::NZ, NV = C::NV, NT = C::NT, NSH = C::NSH;
+    if (ctx->n_q != NS * NZ || ctx->n_shape != NSH) return false;
+    const double* pts = ctx->h_pts.data();
+    const double* phi = ctx->h_phi.data();
+    auto PHI = [&](int q, int k, int dof) { return phi[(static_cast<size_t>(q) * 4 + k) * NSH + dof]; };
+    for (int z = 0; z < NZ; ++z)
+      for (int s = 0; s < NS; ++s) {
+        const int q = z * NS + s;
+        if (pts[3 * q] != pts[3 * s] || pts[3 * q + 1] != pts[3 * s + 1] || pts[3 * q + 2] != pts[3 * z * NS + 2])
+          return false;
+      }
+    tri.assign(2 * NS, 0.0);
+    for (int s = 0; s < NS; ++s) {
+      tri[s] = pts[3 * s];
+      tri[NS + s] = pts[3 * s + 1];
+    }
+    // Y: P_a(z) = phi_0((t=0,a), (s=0,z)), P'_a(z) = phi_3((0,a),(0,z)) since m_0 = 1.
+    yline.assign(2 * NV * NZ + NZ, 0.0);
+    for (int a = 0; a < NV; ++a)
+      for (int z = 0; z < NZ; ++z) {
+        yline[a * NZ + z] = PHI(z * NS, 0, a);
+        yline[NV * NZ + a * NZ + z] = PHI(z * NS, 3, a);
+      }
+    for (int z = 0; z < NZ; ++z) yline[2 * NV * NZ + z] = pts[3 * z * NS + 2];
+    // X_x(t,s): x=0 dm/dxi1, 1 dm/dxi2, 2 m, read at a=0 (P_0 = 1), z=0.
+    std::vector<double> X(static_cast<size_t>(3) * NT * NS);
+    for (int t = 0; t < NT; ++t)
+      for (int s = 0; s < NS; ++s) {
+        X[(0 * NT + t) * NS + s] = PHI(s, 1, t * NV);
+        X[(1 * NT + t) * NS + s] = PHI(s, 2, t * NV);
+        X[(2 * NT + t) * NS + s] = PHI(s, 0, t * NV) / PHI(s, 0, 0);
+      }
+    // Structure check: phi_k(i,q) == X(t,s) Y(a,z) to rounding.
+    double worst = 0.0, scale = 0.0;
+    for (int z = 0; z < NZ; ++z)
+      for (int s = 0; s < NS; ++s)
+        for (int t = 0; t < NT; ++t)
+          for (int a = 0; a < NV; ++a) {
+            const int q = z * NS + s, dof = t * NV + a;
+            const double Pz = yline[a * NZ + z], D = yline[NV * NZ + a * NZ + z];
+            const double m = X[(2 * NT + t) * NS + s];
+            const double ref[4] = {m * Pz, X[(0 * NT + t) * NS + s] * Pz, X[(1 * NT + t) * NS + s] * Pz, m * D};
+            for (int k = 0; k < 4; ++k) {
+              worst = std::max(worst, std::fabs(PHI(q, k, dof) - ref[k]));
+              scale = std::max(scale, std::fabs(ref[k]));
+            }
+          }
+    if (worst > 1e-13 * std::max(1.0, scale)) return false;
+    xfrag.assign(C::XFRAG, 0.0);
+    for (int mt = 0; mt < C::MT; ++mt)
+      for (int ks = 0; ks < C::KSTEPS; ++ks)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int t = mt * 8 + lane / 4, kx = ks * 4 + lane % 4;
+          const int s = kx / 3, x = kx % 3;
+          double v = 0.0;
+          if (t < NT && s < NS) v = X[(x * NT + t) * NS + s];
+          xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
+        }
+    return true;
+  }
+};
+
+template <template <int> class F, typename... Args>
+bool dispatch_p(int p, Args&&... args) {
+  switch (p) {
+    case 2: F<2>::run(args...); return true;
+    case 3: F<3>::run(args...); return true;
+    case 4: F<4>::run(args...); return true;
+    case 5: F<5>::run(args...); return true;
+    case 6: F<6>::run(args...); return true;
+    case 7: F<7>::run(args...); return true;
+    default: return false;
+  }
+}
+
+template <int P>
+struct LaunchOp {
+  static void run(const LaunchArgs& a, const SumFactTables& t, bool general, cudaStream_t s) {
+    SumFactHost<P>::launch(a, t, general, s);
+  }
+};
+template <int P>
+struct AttrOp {
+  static void run() { SumFactHost<P>::set_attrs(); }
+};
+template <int P>
+struct BuildOp {
+  static void run(pi_context* ctx, std::vector<double>& x, std::vector<double>& y, std::vector<double>& t,
+                  bool& ok) {
+    ok = SumFactHost<P>::build(ctx, x, y, t);
+  }
+};
+
+template <typename T>
+pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
+  cudaError_t e = cudaMalloc(dst, std::max<size_t>(sizeof(T), src.size() * sizeof(T)));
+  if (e == cudaSuccess && !src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? PI_OK : cuda_fail(err, e, "upload per-p tables");
+}
+
+int resolve_variant(const pi_context* ctx) {
+  if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
+  if (ctx->p == 1) return PI_VARIANT_DENSE;
+  return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pi_version(void) { return "prism_b200 0.1 (sm_100a)"; }
+
+const char* pi_status_name(pi_status s) {
+  static const char* names[] = {"ok",      "config",          "domain",   "unsupported_degree", "inverted_element",
+                                "capacity", "shared_memory_exhausted", "contract_violation", "io", "cuda"};
+  return (s >= 0 && s <= PI_E_CUDA) ? names[s] : "unknown";
+}
+
+pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, const double* points,
+                            const double* weights, const double* shape_table, pi_context** out,
+                            pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!out) return set_error(err, PI_E_CONTRACT, "pi_context_create: out is NULL");
+  *out = nullptr;
+  if (p < 1 || p > kMaxP)
+    return set_error(err, PI_E_DOMAIN, "approximation order p=%d outside supported range [1, 7]", p);
+  if (n_eq != 1)
+    return set_error(err, PI_E_CONFIG, "n_eq=%d: this build integrates scalar weak forms (n_eq = 1)", n_eq);
+  const int nsh = shape_count(p), nq = quad_count(p);
+  if ((points || weights || shape_table) && !(points && weights && shape_table))
+    return set_error(err, PI_E_CONTRACT, "pi_context_create: pass all of points/weights/shape_table or none");
+  if (points && (n_q != nq || n_shape != nsh))
+    return set_error(err, PI_E_CONFIG, "integrator: tables have n_q=%d n_shape=%d, p=%d needs %d and %d", n_q,
+                     n_shape, p, nq, nsh);
+
+  auto* ctx = new pi_context();
+  ctx->device = device;
+  ctx->p = p;
+  ctx->n_eq = n_eq;
+  ctx->n_q = nq;
+  ctx->n_shape = nsh;
+  ctx->h_pts.resize(3 * nq);
+  ctx->h_w.resize(nq);
+  ctx->h_phi.resize(static_cast<size_t>(nq) * 4 * nsh);
+  if (points) {
+    std::memcpy(ctx->h_pts.data(), points, sizeof(double) * 3 * nq);
+    std::memcpy(ctx->h_w.data(), weights, sizeof(double) * nq);
+    std::memcpy(ctx->h_phi.data(), shape_table, sizeof(double) * ctx->h_phi.size());
+  } else {
+    prism_quadrature(p, ctx->h_pts.data(), ctx->h_w.data());
+    for (int q = 0; q < nq; ++q) shape_values(p, &ctx->h_pts[3 * q], &ctx->h_phi[static_cast<size_t>(q) * 4 * nsh]);
+  }
+
+  pi_status st = PI_OK;
+  auto fail = [&](pi_status s) {
+    pi_context_destroy(ctx);
+    return s;
+  };
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaSetDevice"));
+  ce = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaStreamCreate"));
+  if ((st = upload(&ctx->d_phi, ctx->h_phi, err)) != PI_OK) return fail(st);
+  if ((st = upload(&ctx->d_pts, ctx->h_pts, err)) != PI_OK) return fail(st);
+  if ((st = upload(&ctx->d_w, ctx->h_w, err)) != PI_OK) return fail(st);
+  ce = cudaMalloc(&ctx->d_bad, sizeof(unsigned long long));
+  if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMalloc"));
+  ce = cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long));
+  if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
+
+  if (p >= 2) {
+    std::vector<double> xf, yl, tr;
+    bool ok = false;
+    dispatch_p<BuildOp>(p, ctx, xf, yl, tr, ok);
+    ctx->tensor_ok = ok;
+    if (ok) {
+      if ((st = upload(&ctx->d_xfrag, xf, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_yline, yl, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_tri, tr, err)) != PI_OK) return fail(st);
+      dispatch_p<AttrOp>(p);
+    } else {
+      return fail(set_error(err, PI_E_CONFIG,
+                            "shape table / rule are not the tensor-product prism basis the kernels factorise"));
+    }
+  }
+  ce = cudaGetLastError();
+  if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "context setup"));
+  *out = ctx;
+  return PI_OK;
+}
+
+pi_status pi_context_destroy(pi_context* ctx) {
+  if (!ctx) return PI_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& s : ctx->hs)
+    if (s) cudaStreamDestroy(s);
+  cudaFree(ctx->d_phi);
+  cudaFree(ctx->d_pts);
+  cudaFree(ctx->d_w);
+  cudaFree(ctx->d_xfrag);
+  cudaFree(ctx->d_yline);
+  cudaFree(ctx->d_tri);
+  cudaFree(ctx->d_bad);
+  if (ctx->hbuf) cudaFree(ctx->hbuf);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PI_OK;
+}
+
+pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* err) {
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if (variant < PI_VARIANT_AUTO || variant > PI_VARIANT_SUMFACT)
+    return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
+  if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
+    return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
+  if (variant == PI_VARIANT_DENSE && ctx->p != 1)
+    return set_error(err, PI_E_CONFIG, "dense variant is built for p = 1 only in this release");
+  ctx->variant = variant;
+  return PI_OK;
+}
+
+int pi_context_variant(const pi_context* ctx, int coeff_mode) {
+  (void)coeff_mode;
+  return ctx ? resolve_variant(ctx) : -1;
+}
+
+void* pi_context_stream(pi_context* ctx) { return ctx ? ctx->stream : nullptr; }
+
+pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                       int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
+                       int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if (n_elem < 0) return set_error(err, PI_E_CONTRACT, "n_elem < 0");
+  if (n_elem == 0) return PI_OK;
+  if (!geom || !out) return set_error(err, PI_E_CONTRACT, "geometry/output buffers must be non-NULL");
+  if (geom_ld < n_elem) return set_error(err, PI_E_CONTRACT, "geom_ld (%lld) < n_elem (%lld)", (long long)geom_ld,
+                                         (long long)n_elem);
+  if (out_layout != PI_OUT_CANONICAL && out_layout != PI_OUT_SOA)
+    return set_error(err, PI_E_CONFIG, "unknown output layout %d", out_layout);
+  if (out_layout == PI_OUT_SOA && ld_out < n_elem) return set_error(err, PI_E_CONTRACT, "ld_out < n_elem");
+  LaunchArgs a{};
+  a.n_elem = n_elem;
+  a.element_id_base = element_id_base;
+  a.geom = geom;
+  a.geom_ld = geom_ld;
+  a.out = out;
+  a.out_layout = out_layout;
+  a.ld_out = ld_out;
+  a.bad = ctx->d_bad;
+  bool general = false;
+  switch (coeff_mode) {
+    case PI_COEFF_LAPLACE:
+      break;
+    case PI_COEFF_UNIFORM:
+      if (!coeff) return set_error(err, PI_E_CONTRACT, "uniform coefficient tensor is NULL");
+      std::memcpy(a.cu, coeff, sizeof(a.cu));
+      general = true;
+      break;
+    case PI_COEFF_PER_ELEMENT:
+      if (!coeff || coeff_ld < n_elem) return set_error(err, PI_E_CONTRACT, "per-element coefficients: bad buffer/ld");
+      a.coeff = coeff;
+      a.coeff_ld = coeff_ld;
+      general = true;
+      break;
+    default:
+      return set_error(err, PI_E_CONFIG, "unknown coefficient mode %d", coeff_mode);
+  }
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int v = resolve_variant(ctx);
+  if (v == PI_VARIANT_DENSE) {
+    DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
+    const unsigned grid = static_cast<unsigned>((n_elem + kP1Threads - 1) / kP1Threads);
+    if (general)
+      p1_thread_kernel<true><<<grid, kP1Threads, 0, s>>>(a, t);
+    else
+      p1_thread_kernel<false><<<grid, kP1Threads, 0, s>>>(a, t);
+  } else {
+    SumFactTables t{ctx->d_xfrag, ctx->d_yline, ctx->d_tri, ctx->d_w};
+    dispatch_p<LaunchOp>(ctx->p, a, t, general, s);
+  }
+  PI_CUDA(cudaGetLastError(), "kernel launch");
+  ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
+  if (ctx->calls.size() > 4096) ctx->calls.erase(ctx->calls.begin(), ctx->calls.begin() + 2048);
+  return PI_OK;
+}
+
+pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                          int64_t geom_ld, const double* f, double f_const, double* out, void* stream,
+                          pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
+  if (!geom || !out || geom_ld < n_elem) return set_error(err, PI_E_CONTRACT, "bad geometry/output buffers");
+  LaunchArgs a{};
+  a.n_elem = n_elem;
+  a.element_id_base = element_id_base;
+  a.geom = geom;
+  a.geom_ld = geom_ld;
+  a.out = out;
+  a.bad = ctx->d_bad;
+  DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);
+  load_vector_kernel<<<grid, 32 * kLoadWarps, sizeof(double) * kLoadWarps * ctx->n_q, s>>>(a, t, ctx->n_q,
+                                                                                            ctx->n_shape, f, f_const);
+  PI_CUDA(cudaGetLastError(), "load-vector launch");
+  ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
+  return PI_OK;
+}
+
+pi_status pi_check(pi_context* ctx, pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  PI_CUDA(cudaStreamSynchronize(ctx->stream), "stream synchronize");
+  PI_CUDA(cudaDeviceSynchronize(), "device synchronize");
+  unsigned long long bad = ~0ull;
+  PI_CUDA(cudaMemcpy(&bad, ctx->d_bad, sizeof bad, cudaMemcpyDeviceToHost), "read inverted-element flag");
+  if (bad == ~0ull) {
+    ctx->calls.clear();
+    return PI_OK;
+  }
+  PI_CUDA(cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long)), "reset flag");
+  const int64_t gid = static_cast<int64_t>(bad);
+  // Describe it like InvertedElementError (errors.cpp:33-41): first failing
+  // rule point in rule order, with its determinant.
+  double xi[3] = {0, 0, 0}, det = 0.0;
+  for (auto it = ctx->calls.rbegin(); it != ctx->calls.rend(); ++it) {
+    if (gid < it->base || gid >= it->base + it->n) continue;
+    const int64_t le = gid - it->base;
+    double g[18];
+    bool got = true;
+    for (int c = 0; c < 18; ++c)
+      if (cudaMemcpy(&g[c], it->geom + c * it->ld + le, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        got = false;
+    if (!got) break;
+    for (int q = 0; q < ctx->n_q; ++q) {
+      double inv[9], d;
+      if (!jacobian_terms(g, &ctx->h_pts[3 * q], d, inv)) {
+        std::memcpy(xi, &ctx->h_pts[3 * q], sizeof xi);
+        det = d;
+        break;
+      }
+    }
+    break;
+  }
+  ctx->calls.clear();
+  pi_status st = set_error(err, PI_E_INVERTED_ELEMENT, "inverted element %lld: det=%f at xi=(%f, %f, %f)",
+                           (long long)gid, det, xi[0], xi[1], xi[2]);
+  if (err) {
+    err->element = gid;
+    err->det = det;
+    std::memcpy(err->xi, xi, sizeof xi);
+  }
+  return st;
+}
+
+pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
+                            int coeff_mode, const double* coeff, double* out, int64_t chunk_elems,
+                            pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
+  if (!geom_aos || !out) return set_error(err, PI_E_CONTRACT, "NULL host buffers");
+  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int64_t kk = static_cast<int64_t>(ctx->n_shape) * ctx->n_shape;
+  const int cw = coeff_mode == PI_COEFF_PER_ELEMENT ? 16 : 0;
+  const size_t per_elem = sizeof(double) * (kk + 2 * 18 + 2 * cw);
+  if (chunk_elems <= 0) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t budget = std::min<size_t>(free_b / 4, size_t(4) << 30);  // per slot
+    chunk_elems = std::max<int64_t>(1, static_cast<int64_t>(budget / per_elem));
+  }
+  chunk_elems = std::min(chunk_elems, n_elem);
+  const size_t slot_bytes = per_elem * chunk_elems;
+  if (ctx->hbuf_bytes < 2 * slot_bytes) {
+    if (ctx->hbuf) cudaFree(ctx->hbuf);
+    ctx->hbuf = nullptr;
+    ctx->hbuf_bytes = 0;
+    PI_CUDA(cudaMalloc(&ctx->hbuf, 2 * slot_bytes), "allocate streaming buffers");
+    ctx->hbuf_bytes = 2 * slot_bytes;
+  }
+  for (auto& s : ctx->hs)
+    if (!s) PI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+  int64_t done = 0;
+  int slot = 0;
+  while (done < n_elem) {
+    const int64_t cnt = std::min(chunk_elems, n_elem - done);
+    cudaStream_t s = ctx->hs[slot];
+    double* base = ctx->hbuf + slot * (slot_bytes / sizeof(double));
+    double* d_out = base;
+    double* d_aos = d_out + kk * chunk_elems;
+    double* d_geom = d_aos + 18 * chunk_elems;
+    double* d_caos = d_geom + 18 * chunk_elems;
+    double* d_coef = d_caos + cw * chunk_elems;
+    PI_CUDA(cudaMemcpyAsync(d_aos, geom_aos + 18 * done, sizeof(double) * 18 * cnt, cudaMemcpyHostToDevice, s), "H2D geometry");
+    aos_to_soa_kernel<<<static_cast<unsigned>((18 * cnt + 255) / 256), 256, 0, s>>>(d_aos, d_geom, cnt, 18, cnt);
+    const double* cptr = coeff;
+    int64_t cld = 0;
+    if (cw) {
+      PI_CUDA(cudaMemcpyAsync(d_caos, coeff + 16 * done, sizeof(double) * 16 * cnt, cudaMemcpyHostToDevice, s),
+              "H2D coefficients");
+      aos_to_soa_kernel<<<static_cast<unsigned>((16 * cnt + 255) / 256), 256, 0, s>>>(d_caos, d_coef, cnt, 16, cnt);
+      cptr = d_coef;
+      cld = cnt;
+    }
+    pi_status st = pi_integrate(ctx, cnt, element_id_base + done, d_geom, cnt, coeff_mode, cptr, cld, d_out,
+                                PI_OUT_CANONICAL, 0, s, err);
+    if (st != PI_OK) return st;
+    PI_CUDA(cudaMemcpyAsync(out + kk * done, d_out, sizeof(double) * kk * cnt, cudaMemcpyDeviceToHost, s), "D2H K");
+    done += cnt;
+    slot ^= 1;
+  }
+  PI_CUDA(cudaStreamSynchronize(ctx->hs[0]), "sync");
+  PI_CUDA(cudaStreamSynchronize(ctx->hs[1]), "sync");
+  // Device geometry of the streamed chunks is gone; report by element id.
+  unsigned long long bad = ~0ull;
+  PI_CUDA(cudaMemcpy(&bad, ctx->d_bad, sizeof bad, cudaMemcpyDeviceToHost), "read flag");
+  ctx->calls.clear();
+  if (bad != ~0ull) {
+    PI_CUDA(cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long)), "reset flag");
+    const int64_t gid = static_cast<int64_t>(bad);
+    const double* g = geom_aos + 18 * (gid - element_id_base);
+    double xi[3] = {0, 0, 0}, det = 0.0;
+    for (int q = 0; q < ctx->n_q; ++q) {
+      double inv[9], d;
+      if (!jacobian_terms(g, &ctx->h_pts[3 * q], d, inv)) {
+        std::memcpy(xi, &ctx->h_pts[3 * q], sizeof xi);
+        det = d;
+        break;
+      }
+    }
+    pi_status st = set_error(err, PI_E_INVERTED_ELEMENT, "inverted element %lld: det=%f at xi=(%f, %f, %f)",
+                             (long long)gid, det, xi[0], xi[1], xi[2]);
+    if (err) {
+      err->element = gid;
+      err->det = det;
+      std::memcpy(err->xi, xi, sizeof xi);
+    }
+    return st;
+  }
+  return PI_OK;
+}
+
+double pi_flops_dense_per_element(int p, int n_eq, int coeff_mode) {
+  (void)n_eq;
+  const double nsh = shape_count(p), nq = quad_count(p);
+  const double r = coeff_mode == PI_COEFF_LAPLACE ? 3.0 : 4.0;
+  return nq * (2.0 * r * nsh * nsh + (2.0 * r * r + 15.0) * nsh + 151.0);
+}
+
+double pi_bytes_per_element(int p, int n_eq, int coeff_mode) {
+  const double dim = static_cast<double>(n_eq) * shape_count(p);
+  return 8.0 * dim * dim + 144.0 + (coeff_mode == PI_COEFF_PER_ELEMENT ? 128.0 * n_eq * n_eq : 0.0);
+}
+
+double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
+  if (!ctx) return 0.0;
+  const int p = ctx->p;
+  const bool general = coeff_mode != PI_COEFF_LAPLACE;
+  const double nq = quad_count(p), nsh = shape_count(p);
+  // Per rule point: Jacobian 57, cofactor inverse 42, det*w 1, M block
+  // 36 (Laplace) / 136 (general).
+  const double per_point = 100.0 + (general ? 136.0 : 36.0);
+  if (resolve_variant(ctx) == PI_VARIANT_DENSE) {
+    // G_l(i) = sum_k phi_k M_kl and K_ij += sum_l G_l phi_l (upper triangle for Laplace).
+    const double r = general ? 4.0 : 3.0;
+    const double pairs = general ? nsh * nsh : nsh * (nsh + 1) / 2;
+    return nq * (per_point + 2.0 * r * r * nsh + 2.0 * r * pairs);
+  }
+  const double nv = p + 1, nt = (p + 1) * (p + 2) / 2.0, ns = tri_point_count(p), nz = p + 1;
+  const double h_terms = general ? 16.0 / 9.0 : 1.0;
+  const double h = ns * nv * nv * 9.0 * nz * 3.0 * h_terms;
+  const double g = ns * 3.0 * nv * nsh * 3.0 * 2.0;
+  const double k = nt * 3.0 * ns * nsh * nv * 2.0;
+  return nq * per_point + h + g + k;
+}
+
+}  // extern "C"

@@ -1,0 +1,230 @@
+"""ctypes wrappers over the CHECKERS (test infrastructure only).
+
+* ``Oracle``    -- oracle/liboracle.so, the plain-C restatement of the reference
+                   arithmetic (oracle/prism_oracle.c).
+* ``Reference`` -- oracle/_ref/libprismint_ref.so, the unmodified reference
+                   sources compiled by oracle/Makefile (absent when the
+                   reference tree was not available at build time).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+ORACLE_SO = ROOT / "oracle" / "liboracle.so"
+REF_SO = ROOT / "oracle" / "_ref" / "libprismint_ref.so"
+
+_dp = C.POINTER(C.c_double)
+
+
+def _ptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def shape_count(p: int) -> int:
+    return (p + 1) * (p + 1) * (p + 2) // 2
+
+
+QUAD_COUNTS = {1: 6, 2: 18, 3: 48, 4: 80, 5: 150, 6: 231, 7: 336}
+
+
+class Oracle:
+    def __init__(self, path: Path = ORACLE_SO):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        self.lib = C.CDLL(str(path))
+        L = self.lib
+        L.po_integrate_generic.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.POINTER(C.c_int)]
+        L.po_load_vector.argtypes = [C.c_int, _dp, C.c_double, _dp]
+        L.po_generate_box_mesh.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, _dp]
+        L.po_prism_quadrature.argtypes = [C.c_int, _dp, _dp]
+        L.po_tabulate_shapes.argtypes = [C.c_int, _dp]
+        L.po_jacobian_terms.argtypes = [_dp, _dp, _dp, _dp]
+        L.po_elasticity_tensor.argtypes = [C.c_double, C.c_double, _dp]
+        L.po_gauss_legendre.argtypes = [C.c_int, _dp, _dp]
+        L.po_triangle_rule.argtypes = [C.c_int, _dp, _dp]
+
+    def quadrature(self, p):
+        nq = QUAD_COUNTS[p]
+        pts = np.zeros((nq, 3))
+        w = np.zeros(nq)
+        assert self.lib.po_prism_quadrature(p, _ptr(pts), _ptr(w)) == nq
+        return pts, w
+
+    def shape_table(self, p):
+        t = np.zeros((QUAD_COUNTS[p], 4, shape_count(p)))
+        assert self.lib.po_tabulate_shapes(p, _ptr(t)) == 0
+        return t
+
+    def triangle_rule(self, degree):
+        pts = np.zeros((64, 2))
+        w = np.zeros(64)
+        n = self.lib.po_triangle_rule(degree, _ptr(pts), _ptr(w))
+        if n < 0:
+            raise ValueError(f"unsupported degree {degree}")
+        return pts[:n].copy(), w[:n].copy()
+
+    def gauss_legendre(self, n):
+        x = np.zeros(n)
+        w = np.zeros(n)
+        self.lib.po_gauss_legendre(n, _ptr(x), _ptr(w))
+        return x, w
+
+    def jacobian_terms(self, geom, xi):
+        geom = np.ascontiguousarray(geom, dtype=np.float64).reshape(18)
+        xi = np.ascontiguousarray(xi, dtype=np.float64)
+        det = np.zeros(1)
+        inv = np.zeros(9)
+        rc = self.lib.po_jacobian_terms(_ptr(geom), _ptr(xi), _ptr(det), _ptr(inv))
+        return rc, det[0], inv.reshape(3, 3)
+
+    def integrate_generic(self, p, geom, coeff, n_eq=1):
+        """One element; geom [6][3], coeff [n_eq][n_eq][4][4]. Raises on inversion."""
+        geom = np.ascontiguousarray(geom, dtype=np.float64).reshape(18)
+        coeff = np.ascontiguousarray(coeff, dtype=np.float64).reshape(n_eq * n_eq * 16)
+        dim = n_eq * shape_count(p)
+        out = np.zeros((dim, dim))
+        bad = C.c_int(-1)
+        rc = self.lib.po_integrate_generic(p, n_eq, _ptr(geom), _ptr(coeff), _ptr(out), C.byref(bad))
+        if rc == 1:
+            raise InvertedElement(bad.value)
+        assert rc == 0
+        return out
+
+    def integrate_batch(self, p, geoms, coeffs, n_eq=1):
+        """geoms [E][6][3]; coeffs [E][...] or a single tensor."""
+        geoms = np.asarray(geoms, dtype=np.float64).reshape(-1, 18)
+        coeffs = np.asarray(coeffs, dtype=np.float64).reshape(-1, n_eq * n_eq * 16)
+        out = [
+            self.integrate_generic(p, geoms[e], coeffs[e if len(coeffs) > 1 else 0], n_eq)
+            for e in range(len(geoms))
+        ]
+        return np.stack(out)
+
+    def load_vector(self, p, geom, f):
+        geom = np.ascontiguousarray(geom, dtype=np.float64).reshape(18)
+        out = np.zeros(shape_count(p))
+        assert self.lib.po_load_vector(p, _ptr(geom), float(f), _ptr(out)) == 0
+        return out
+
+    def box_mesh(self, nx, ny, nz, distortion, seed):
+        out = np.zeros((2 * nx * ny * nz, 6, 3))
+        assert self.lib.po_generate_box_mesh(nx, ny, nz, distortion, seed, _ptr(out)) == 0
+        return out
+
+    def elasticity_tensor(self, young, nu):
+        out = np.zeros((3, 3, 4, 4))
+        assert self.lib.po_elasticity_tensor(young, nu, _ptr(out)) == 0
+        return out
+
+
+class InvertedElement(Exception):
+    def __init__(self, where):
+        super().__init__(f"inverted element at {where}")
+        self.where = where
+
+
+class RefError(C.Structure):
+    _fields_ = [("code", C.c_int), ("element", C.c_int64), ("det", C.c_double),
+                ("message", C.c_char * 256)]
+
+
+class Reference:
+    """The reference's own arithmetic (oracle/_ref)."""
+
+    def __init__(self, path: Path = REF_SO):
+        if not path.exists():
+            raise FileNotFoundError(f"{path} missing (reference not built here)")
+        self.lib = C.CDLL(str(path))
+        L = self.lib
+        L.ref_prism_quadrature.argtypes = [C.c_int, _dp, _dp, C.POINTER(RefError)]
+        L.ref_tabulate_shapes.argtypes = [C.c_int, _dp, C.POINTER(RefError)]
+        L.ref_generate_box_mesh.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, _dp,
+                                            C.POINTER(RefError)]
+        L.ref_integrate_generic_batch.argtypes = [C.c_int, C.c_int, C.c_int64, _dp, _dp, C.c_int, _dp,
+                                                  C.c_int64, C.c_int, C.POINTER(RefError)]
+        L.ref_integrate_optimized.argtypes = [C.c_int, _dp, C.c_double, C.c_double, _dp,
+                                              C.POINTER(RefError)]
+        L.ref_jacobian_terms.argtypes = [_dp, _dp, _dp, _dp, C.c_int64, C.POINTER(RefError)]
+        L.ref_gauss_legendre.argtypes = [C.c_int, _dp, _dp, C.POINTER(RefError)]
+        L.ref_triangle_rule.argtypes = [C.c_int, _dp, _dp, C.POINTER(RefError)]
+        L.ref_elasticity_tensor.argtypes = [C.c_double, C.c_double, _dp, C.POINTER(RefError)]
+
+    def _check(self, rc, err):
+        if rc != 0:
+            raise RuntimeError(f"reference error code {rc}: {err.message.decode()} (element {err.element})")
+
+    def quadrature(self, p):
+        nq = QUAD_COUNTS[p]
+        pts = np.zeros((nq, 3))
+        w = np.zeros(nq)
+        err = RefError()
+        self._check(self.lib.ref_prism_quadrature(p, _ptr(pts), _ptr(w), C.byref(err)), err)
+        return pts, w
+
+    def shape_table(self, p):
+        t = np.zeros((QUAD_COUNTS[p], 4, shape_count(p)))
+        err = RefError()
+        self._check(self.lib.ref_tabulate_shapes(p, _ptr(t), C.byref(err)), err)
+        return t
+
+    def box_mesh(self, nx, ny, nz, distortion, seed):
+        out = np.zeros((2 * nx * ny * nz, 6, 3))
+        err = RefError()
+        self._check(self.lib.ref_generate_box_mesh(nx, ny, nz, distortion, seed, _ptr(out), C.byref(err)), err)
+        return out
+
+    def integrate_batch(self, p, geoms, coeffs, n_eq=1, threads=0, element_id_base=0):
+        """Returns (out [E][dim][dim], err) ; err is None or a RefError."""
+        geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1, n_eq * n_eq * 16)
+        per_el = 1 if len(coeffs) > 1 else 0
+        dim = n_eq * shape_count(p)
+        out = np.zeros((len(geoms), dim, dim))
+        err = RefError()
+        rc = self.lib.ref_integrate_generic_batch(p, n_eq, len(geoms), _ptr(geoms), _ptr(coeffs), per_el,
+                                                  _ptr(out), element_id_base, threads, C.byref(err))
+        return out, (err if rc else None)
+
+    def integrate_optimized(self, p, geom, young, nu):
+        geom = np.ascontiguousarray(geom, dtype=np.float64).reshape(18)
+        dim = 3 * shape_count(p)
+        out = np.zeros((dim, dim))
+        err = RefError()
+        self._check(self.lib.ref_integrate_optimized(p, _ptr(geom), young, nu, _ptr(out), C.byref(err)), err)
+        return out
+
+
+def rel_frobenius(ref: np.ndarray, other: np.ndarray, axis=None) -> np.ndarray:
+    """verify.cpp:461-469 / oracles.cpp:163-172: sqrt(sum (a-b)^2 / sum a^2)."""
+    ref = np.asarray(ref)
+    other = np.asarray(other)
+    if axis is None:
+        num = np.sum((ref - other) ** 2)
+        den = np.sum(ref * ref)
+        return np.sqrt(num / den) if den > 0 else np.sqrt(num)
+    num = np.sum((ref - other) ** 2, axis=axis)
+    den = np.sum(ref * ref, axis=axis)
+    return np.where(den > 0, np.sqrt(num / np.where(den > 0, den, 1)), np.sqrt(num))
+
+
+def sample_indices(n: int, want: int):
+    """verify.cpp:50-59: evenly spaced sample."""
+    if n == 0:
+        return []
+    want = min(want, n)
+    return [0 if want == 1 else i * (n - 1) // (want - 1) for i in range(want)]
+
+
+def laplace_tensor():
+    c = np.zeros((1, 1, 4, 4))
+    for d in range(1, 4):
+        c[0, 0, d, d] = 1.0
+    return c
