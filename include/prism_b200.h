@@ -148,6 +148,10 @@ double pi_flops_dense_per_element(int p, int n_eq, int coeff_mode);
 double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode);
 double pi_bytes_per_element(int p, int n_eq, int coeff_mode);
 
+/* Diagnostics: measured FP64 tensor-pipe (DMMA m8n8k4) and FMA-pipe peaks in
+ * TFLOP/s on `device` -- the FP64 roofline denominators.  Returns 0 on success. */
+int pi_measure_fp64_peak(int device, double* dmma_tflops, double* dfma_tflops);
+
 const char* pi_status_name(pi_status s);
 const char* pi_version(void);
 

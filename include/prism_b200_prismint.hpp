@@ -1,0 +1,145 @@
+// include/prism_b200_prismint.hpp -- header-only C++ shim that lets prismint
+// (the reference, /root/reference/proj) call the B200 kernels with its own
+// types.  Include it from reference code and link libprism_b200.so:
+//
+//   #include "prismint/integrate_ref.hpp"
+//   #include "prism_b200_prismint.hpp"
+//   auto mats = prism_b200::run_batch(p, mesh, coeffs);       // kernels.cpp:485 shape
+//   auto same = prism_b200::integrate_batch(mesh, coeffs, shapes, rule);
+//
+// Semantics: integrate_generic (integrate_ref.cpp:50-91) per element, in mesh
+// order, element-constant coefficients (coefficients_at_point is the
+// identity, coefficients.cpp:61-66).  Errors come back as the reference's own
+// exception classes (errors.hpp:10-85), InvertedElementError naming the
+// global element id base + index like kernels.cpp:158,249.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "prism_b200.h"
+#include "prismint/coefficients.hpp"
+#include "prismint/errors.hpp"
+#include "prismint/geometry.hpp"
+#include "prismint/integrate_ref.hpp"
+#include "prismint/reference_element.hpp"
+
+namespace prism_b200 {
+
+/// Maps a pi_status to the matching prismint exception.
+[[noreturn]] inline void throw_status(pi_status s, const pi_error_info& e) {
+  const std::string msg(e.message);
+  switch (s) {
+    case PI_E_CONFIG: throw prismint::ConfigError(msg);
+    case PI_E_DOMAIN: throw prismint::DomainError(msg);
+    case PI_E_UNSUPPORTED_DEGREE: throw prismint::UnsupportedDegreeError(msg);
+    case PI_E_INVERTED_ELEMENT:
+      throw prismint::InvertedElementError(e.element, e.xi[0], e.xi[1], e.xi[2], e.det);
+    case PI_E_CAPACITY: throw prismint::CapacityError(msg);
+    case PI_E_SHARED_MEMORY: throw prismint::SharedMemoryError(msg);
+    case PI_E_CONTRACT: throw prismint::ContractViolation(msg);
+    case PI_E_IO: throw prismint::IoError(msg);
+    default: throw std::runtime_error("prism_b200: " + msg);
+  }
+}
+
+inline void check(pi_status s, const pi_error_info& e) {
+  if (s != PI_OK) throw_status(s, e);
+}
+
+/// RAII context over pi_context_create with the reference's own rule and
+/// shape table (the constants run_batch builds, kernels.cpp:493-494).
+class Context {
+ public:
+  Context(const prismint::ShapeTable& shapes, const prismint::QuadratureRule& rule, int n_eq = 1, int device = 0) {
+    if (shapes.order_p != rule.order_p || shapes.per_point.size() != rule.points.size())
+      throw prismint::ConfigError("prism_b200: shape table and rule disagree");
+    const int nq = rule.size(), nsh = shapes.n_shape;
+    std::vector<double> pts(3 * nq), tab(static_cast<std::size_t>(nq) * 4 * nsh);
+    for (int q = 0; q < nq; ++q) {
+      pts[3 * q] = rule.points[q].xi1;
+      pts[3 * q + 1] = rule.points[q].xi2;
+      pts[3 * q + 2] = rule.points[q].xi3;
+      std::memcpy(&tab[static_cast<std::size_t>(q) * 4 * nsh], shapes.per_point[q].data.data(),
+                  sizeof(double) * 4 * nsh);
+    }
+    pi_error_info e{};
+    check(pi_context_create(device, rule.order_p, n_eq, nq, nsh, pts.data(), rule.weights.data(), tab.data(),
+                            &ctx_, &e),
+          e);
+    p_ = rule.order_p;
+    n_eq_ = n_eq;
+    nsh_ = nsh;
+  }
+  ~Context() { pi_context_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  /// Whole mesh through the host-buffer path; coefficients: one tensor for
+  /// all elements, or one per element.
+  std::vector<prismint::ElementStiffness> integrate(std::span<const prismint::PrismGeometry> mesh,
+                                                    std::span<const prismint::CoefficientTensor> coeffs,
+                                                    std::int64_t element_id_base = 0) {
+    if (coeffs.empty() || (coeffs.size() != 1 && coeffs.size() != mesh.size()))
+      throw prismint::ConfigError("prism_b200: need one coefficient tensor or one per element");
+    for (const auto& c : coeffs)
+      if (c.n_eq != n_eq_) throw prismint::ConfigError("prism_b200: coefficient n_eq mismatch");
+    const std::size_t n = mesh.size();
+    std::vector<double> geom(18 * n);
+    for (std::size_t e = 0; e < n; ++e)
+      for (int v = 0; v < 6; ++v)
+        for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
+    const int nc = 16 * n_eq_ * n_eq_;
+    std::vector<double> cbuf(coeffs.size() * nc);
+    for (std::size_t k = 0; k < coeffs.size(); ++k)
+      std::memcpy(&cbuf[k * nc], coeffs[k].entries.data(), sizeof(double) * nc);
+    const int mode = coeffs.size() == 1 ? PI_COEFF_UNIFORM : PI_COEFF_PER_ELEMENT;
+    const std::size_t kk = static_cast<std::size_t>(nsh_) * n_eq_ * nsh_ * n_eq_;
+    std::vector<double> out(kk * n);
+    pi_error_info e{};
+    check(pi_integrate_host(ctx_, static_cast<std::int64_t>(n), element_id_base, geom.data(), mode, cbuf.data(),
+                            out.data(), 0, &e),
+          e);
+    std::vector<prismint::ElementStiffness> res(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      auto& a = res[i];
+      a.order_p = p_;
+      a.n_eq = n_eq_;
+      a.n_shape = nsh_;
+      a.data.assign(out.begin() + i * kk, out.begin() + (i + 1) * kk);
+    }
+    return res;
+  }
+
+  pi_context* raw() { return ctx_; }
+
+ private:
+  pi_context* ctx_ = nullptr;
+  int p_ = 0, n_eq_ = 1, nsh_ = 0;
+};
+
+/// integrate_generic for a whole mesh (mesh order), the reference's tables.
+inline std::vector<prismint::ElementStiffness> integrate_batch(std::span<const prismint::PrismGeometry> mesh,
+                                                               std::span<const prismint::CoefficientTensor> coeffs,
+                                                               const prismint::ShapeTable& shapes,
+                                                               const prismint::QuadratureRule& rule, int device = 0,
+                                                               std::int64_t element_id_base = 0) {
+  Context ctx(shapes, rule, coeffs.empty() ? 1 : coeffs.front().n_eq, device);
+  return ctx.integrate(mesh, coeffs, element_id_base);
+}
+
+/// run_batch-shaped entry (kernels.hpp:73-75): builds the rule and table like
+/// the reference does, integrates the mesh with one coefficient tensor.
+inline std::vector<prismint::ElementStiffness> run_batch(int p, std::span<const prismint::PrismGeometry> mesh,
+                                                         const prismint::CoefficientTensor& coeff, int device = 0) {
+  if (mesh.empty()) throw prismint::ConfigError("run_batch: empty mesh");
+  const prismint::QuadratureRule rule = prismint::prism_quadrature(p);
+  const prismint::ShapeTable shapes = prismint::tabulate_shapes(p, rule);
+  return integrate_batch(mesh, std::span<const prismint::CoefficientTensor>(&coeff, 1), shapes, rule, device);
+}
+
+}  // namespace prism_b200

@@ -31,7 +31,7 @@ __all__ = [
     "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
     "generate_box_mesh", "generate_cdr_coefficients", "laplace_tensor",
-    "Integrator", "run_batch", "flops_dense_per_element", "bytes_per_element", "library",
+    "Integrator", "run_batch", "measure_fp64_peak", "flops_dense_per_element", "bytes_per_element", "library",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -139,6 +139,7 @@ def library():
     L.pi_flops_executed_per_element.restype = C.c_double
     L.pi_bytes_per_element.argtypes = [C.c_int, C.c_int, C.c_int]
     L.pi_bytes_per_element.restype = C.c_double
+    L.pi_measure_fp64_peak.argtypes = [C.c_int, _dp, _dp]
     L.pi_status_name.restype = C.c_char_p
     L.pi_version.restype = C.c_char_p
     _lib = L
@@ -250,6 +251,15 @@ def bytes_per_element(p, coeff_mode=LAPLACE, n_eq=1):
     return library().pi_bytes_per_element(p, n_eq, coeff_mode)
 
 
+def measure_fp64_peak(device=0):
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the device."""
+    a = C.c_double()
+    b = C.c_double()
+    if library().pi_measure_fp64_peak(device, C.byref(a), C.byref(b)) != 0:
+        raise CudaError("FP64 peak probe failed")
+    return a.value, b.value
+
+
 class Integrator:
     """One context: device + p (+ the rule / shape table, the reference's own if given)."""
 
@@ -262,13 +272,17 @@ class Integrator:
         self.dim = n_eq * self.n_shape
         self._keep = []
         args = [None, None, None]
+        n_q, n_shape = self.n_q, self.n_shape
         if points is not None:
             arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (points, weights, shape_table)]
             self._keep = arrs
             args = [_ptr(a) for a in arrs]
+            n_q, n_shape = len(arrs[0]), arrs[2].shape[-1]
+            if arrs[2].size != n_q * 4 * n_shape or arrs[1].size != n_q:
+                raise ContractViolation("rule / shape table sizes are inconsistent")
         h = C.c_void_p()
         err = _ErrInfo()
-        _raise(L.pi_context_create(device, p, n_eq, self.n_q, self.n_shape, *args, C.byref(h), C.byref(err)), err)
+        _raise(L.pi_context_create(device, p, n_eq, n_q, n_shape, *args, C.byref(h), C.byref(err)), err)
         self._h = h
         if variant != VARIANT_AUTO:
             self.set_variant(variant)

@@ -12,10 +12,16 @@
 //     G_x(s,a,j)  = sum_y H_xy(s,a,b_j) X_y(t'_j, s)          j = t'*(p+1)+b
 //     K[(t,a), j] = sum_(s,x) X_x(t,s) G_x(s,a,j)             <- DMMA GEMM
 // with M = T (det w C) T^T the per-point 4x4 block (kernels_common.cuh).
-// Only the last line is O(N_sh^2 N_s); it runs as m8n8k4 FP64 MMAs with the
-// element-independent X table as the A operand (staged once per CTA in
-// fragment order) and G (element-specific) staged per chunk of 4 triangle
-// points in fragment order by the warp that consumes it.
+//
+// Warp specialisation inside each CTA:
+//  * producer warps, per chunk of 4 triangle points: Jacobians and M for the
+//    chunk's points, then H -> shared memory (double buffered, named
+//    barriers FULL/EMPTY);
+//  * consumer warps own accumulator fragments K[t][(a, j)] (all m-tiles of
+//    the element-independent X operand, NB n-tiles, WA rows a).  Each lane
+//    computes exactly the B-fragment value G[k][j] its own m8n8k4 FP64 MMA
+//    consumes (3 FMAs from H and X in shared memory), so G never touches
+//    memory; the A fragments (X) are staged once per CTA in fragment order.
 #pragma once
 
 #include "kernels_common.cuh"
@@ -33,69 +39,89 @@ struct SumFactShape {
   static constexpr int NQ = NS * NZ;
   static constexpr int MT = (NT + 7) / 8;             // m-tiles of the X operand
   static constexpr int NTILE = (NSH + 7) / 8;         // n-tiles of one K row block
+  static constexpr int NTP = (NTILE * 8 + NV - 1) / NV;  // t' range covered by padded columns
   static constexpr int KSTEPS = 3 * NSP / 4;          // k4-steps over (s, x)
   static constexpr int NCHUNK = NSP / 4;              // 4 triangle points per chunk
   static constexpr int XFRAG = MT * KSTEPS * 32;      // doubles in the A-fragment table
+  static constexpr int XPLAIN = NSP * NTP * 4;        // X as [s][t'][y(4)]
 };
 
-// Launch shape: EPC elements x AG Legendre rows `a` per CTA; each warp owns
-// WA rows a x NB n-tiles x all MT m-tiles of accumulators (WA*NB*MT frags).
+// Launch shape: EPC elements x AG Legendre rows `a` per CTA; each consumer
+// warp owns WA rows a x NB n-tiles x all MT m-tiles (WA*NB*MT fragments);
+// NPW producer warps.
 template <int P>
 struct SumFactLaunch;
-template <> struct SumFactLaunch<2> { static constexpr int EPC = 8, AG = 3, WA = 3, NB = 3; };
-template <> struct SumFactLaunch<3> { static constexpr int EPC = 4, AG = 4, WA = 2, NB = 5; };
-template <> struct SumFactLaunch<4> { static constexpr int EPC = 2, AG = 5, WA = 1, NB = 10; };
-template <> struct SumFactLaunch<5> { static constexpr int EPC = 1, AG = 6, WA = 1, NB = 8; };
-template <> struct SumFactLaunch<6> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 5; };
-template <> struct SumFactLaunch<7> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 4; };
+template <> struct SumFactLaunch<2> { static constexpr int EPC = 8, AG = 3, WA = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 2; };
+template <> struct SumFactLaunch<3> { static constexpr int EPC = 4, AG = 4, WA = 2, NB = 5, NPW = 4, BSPLIT = 1, MINB = 1; };
+template <> struct SumFactLaunch<4> { static constexpr int EPC = 1, AG = 5, WA = 1, NB = 10, NPW = 2, BSPLIT = 1, MINB = 2; };
+template <> struct SumFactLaunch<5> { static constexpr int EPC = 1, AG = 3, WA = 1, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1; };
+template <> struct SumFactLaunch<6> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1; };
+template <> struct SumFactLaunch<7> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1; };
 
 template <int P>
 struct SumFactConfig : SumFactShape<P>, SumFactLaunch<P> {
   using S = SumFactShape<P>;
   using L = SumFactLaunch<P>;
-  static constexpr int NBLK = (S::NTILE + L::NB - 1) / L::NB;
-  static constexpr int WPE = (L::AG / L::WA) * NBLK;   // warps per element
-  static constexpr int NWARPS = L::EPC * WPE;
+  static constexpr int NBLK = S::NTILE / L::NB;
+  static constexpr int WPE = (L::AG / L::WA) * NBLK;   // consumer warps per element
+  static constexpr int NCW = L::EPC * WPE;
+  static constexpr int NWARPS = NCW + L::NPW;
   static constexpr int NTHREADS = 32 * NWARPS;
+  static constexpr int NPT = 32 * L::NPW;              // producer threads
   static constexpr int NAG = S::NV / L::AG;            // CTAs per element group
+  static constexpr int BPER = (S::NV + L::BSPLIT - 1) / L::BSPLIT;  // b values per H item
+  // Along a consumer lane's n-tiles, b = (8*nb + lane/4) mod NV repeats with
+  // period R = NV / gcd(8, NV); its H values are cached in registers.
+  static constexpr int R = S::NV / (S::NV % 8 == 0 ? 8 : S::NV % 4 == 0 ? 4 : S::NV % 2 == 0 ? 2 : 1);
+  static constexpr int RC = R < L::NB ? R : L::NB;     // distinct b values a lane touches
   static_assert(S::NV % L::AG == 0 && L::AG % L::WA == 0, "bad a-grouping");
   static_assert(S::NTILE % L::NB == 0, "n-tiles must split evenly");
-  // shared memory layout (doubles)
-  static constexpr int OFF_X = 0;
-  static constexpr int OFF_M = OFF_X + S::XFRAG;
-  static constexpr int OFF_H = OFF_M + L::EPC * S::NQ * 16;
-  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NV * 9;
-  static constexpr int OFF_G = OFF_H + 2 * H_PER_BUF;
-  static constexpr int G_PER_WARP = L::WA * L::NB * 3 * 32;
-  static constexpr int OFF_GEOM = OFF_G + NWARPS * G_PER_WARP;
+  // H for one chunk: [EPC][AG][4 s][NV b][3 x][4 y (padded)]
+  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NV * 12;
+  static constexpr int M_PER_CHUNK = L::EPC * 4 * S::NZ * 16;
+  // shared memory layout (doubles; every block 16-byte aligned)
+  static constexpr int OFF_XA = 0;
+  static constexpr int OFF_XP = OFF_XA + S::XFRAG;
+  static constexpr int OFF_H = OFF_XP + S::XPLAIN;
+  static constexpr int OFF_M = OFF_H + 2 * H_PER_BUF;
+  static constexpr int OFF_GEOM = OFF_M + M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + L::EPC * 18;
-  static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // Y tables [2][NV][NZ], xi3 [NZ]
-  static constexpr int OFF_TRI = OFF_LINE + 2 * S::NV * S::NZ + S::NZ;  // xi1, xi2 [NS]
-  static constexpr int OFF_W = OFF_TRI + 2 * S::NS;                     // weights [NQ]
+  static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
+  static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
+  static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
   static constexpr int SMEM_DOUBLES = OFF_W + S::NQ;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
 };
 
 // Per-p constant tables in device memory (built by the host from the shape
-// table, pi_context.cu): X in A-fragment order, Y = (P, P') at GL points,
-// the triangle and line coordinates, and the rule weights in rule order.
+// table, pi_context.cu).
 struct SumFactTables {
-  const double* xfrag;  // [MT][KSTEPS][32]
-  const double* yline;  // [2][NV][NZ] then xi3 [NZ]
-  const double* tri;    // [2][NS]: xi1 then xi2
-  const double* w;      // [NQ]
+  const double* xfrag;   // X in A-fragment order [MT][KSTEPS][32]
+  const double* xplain;  // X as [NSP][NTP][4] (y = 0..2, zero padded)
+  const double* yline;   // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
+  const double* tri;     // xi1 [NS], xi2 [NS]
+  const double* w;       // [NQ] rule weights (reference order)
 };
 
+// Named barriers (id 0 is __syncthreads).
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProd = 5;
+
 template <int P, bool GENERAL>
-__global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS)
+__global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::MINB)
     sumfact_kernel(LaunchArgs args, SumFactTables tab) {
   using C = SumFactConfig<P>;
-  constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ;
+  constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ, NTP = C::NTP;
   constexpr int MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
+  constexpr int NCHUNK = C::NCHUNK;
   extern __shared__ __align__(16) double smem[];
-  double* sX = smem + C::OFF_X;
-  double* sM = smem + C::OFF_M;
+  double* sXA = smem + C::OFF_XA;
+  double* sXP = smem + C::OFF_XP;
   double* sH = smem + C::OFF_H;
+  double* sM = smem + C::OFF_M;
   double* sGeom = smem + C::OFF_GEOM;
   double* sC = smem + C::OFF_C;
   double* sY = smem + C::OFF_LINE;
@@ -107,8 +133,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS)
   const int agroup = blockIdx.x % C::NAG;
   const int64_t e0 = egroup * EPC;
 
-  // ---- stage per-p tables and per-element inputs ----
-  for (int i = tid; i < C::XFRAG; i += C::NTHREADS) sX[i] = tab.xfrag[i];
+  // ---- stage per-p tables and per-element inputs (all warps) ----
+  for (int i = tid; i < C::XFRAG; i += C::NTHREADS) sXA[i] = tab.xfrag[i];
+  for (int i = tid; i < C::XPLAIN; i += C::NTHREADS) sXP[i] = tab.xplain[i];
   for (int i = tid; i < 2 * NV * NZ + NZ; i += C::NTHREADS) sY[i] = tab.yline[i];
   for (int i = tid; i < 2 * NS; i += C::NTHREADS) sTri[i] = tab.tri[i];
   for (int i = tid; i < NQ; i += C::NTHREADS) sW[i] = tab.w[i];
@@ -128,27 +155,107 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS)
   }
   __syncthreads();
 
-  // ---- M(s,z) for every rule point of every element of the CTA ----
-  for (int i = tid; i < EPC * NQ; i += C::NTHREADS) {
-    const int el = i / NQ, q = i % NQ;
-    const int s = q % NS, z = q / NS;
-    double inv[3][3];
-    const double det = prism_jacobian(sGeom + 18 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], inv);
-    const int64_t e = e0 + el;
-    if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
-    double M[16];
-    coefficient_block<GENERAL>(inv, det * sW[q], sC + 16 * el, M);
-    double* dst = sM + (el * NQ + q) * 16;
+  const double* Pv = sY;            // P_a(z)  [NV][NZ]
+  const double* Pd = sY + NV * NZ;  // P'_a(z) [NV][NZ]
+
+  if (warp >= C::NCW) {
+    // ======================= producer warps =======================
+    const int ptid = tid - 32 * C::NCW;
+    for (int chunk = 0; chunk < NCHUNK; ++chunk) {
+      // (1) M for the chunk's points: (el, sl, z)
+      for (int i = ptid; i < EPC * 4 * NZ; i += C::NPT) {
+        const int z = i % NZ, sl = (i / NZ) % 4, el = i / (4 * NZ);
+        const int s = chunk * 4 + sl;
+        double M[16];
+        if (s < NS) {
+          double inv[3][3];
+          const double det = prism_jacobian(sGeom + 18 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], inv);
+          const int64_t e = e0 + el;
+          if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
+          coefficient_block<GENERAL>(inv, det * sW[z * NS + s], sC + 16 * el, M);
+        } else {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) dst[k] = M[k];
+          for (int k = 0; k < 16; ++k) M[k] = 0.0;
+        }
+        double2* dst = reinterpret_cast<double2*>(sM + i * 16);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dst[k] = make_double2(M[2 * k], M[2 * k + 1]);
+      }
+      named_sync(kBarProd, C::NPT);
+      if (chunk >= 2) named_sync(kBarEmpty0 + (chunk & 1), C::NTHREADS);  // consumers released this buffer
+      double* Hb = sH + (chunk & 1) * C::H_PER_BUF;
+      // (2) H_x,y(s,a,b), y = 0..2: items (el, al, sl, x, b-group), b looped
+      for (int i = ptid; i < EPC * AG * 4 * 3 * C::BSPLIT; i += C::NPT) {
+        const int bg = i % C::BSPLIT, x = (i / C::BSPLIT) % 3, sl = (i / (3 * C::BSPLIT)) % 4;
+        const int al = (i / (12 * C::BSPLIT)) % AG, el = i / (12 * C::BSPLIT * AG);
+        const int a = agroup * AG + al;
+        const int kx = x < 2 ? x + 1 : 3;
+        double h[C::BPER][3];
+#pragma unroll
+        for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
+        const double* Mp = sM + (el * 4 + sl) * NZ * 16;
+#pragma unroll
+        for (int z = 0; z < NZ; ++z) {
+          const double* M = Mp + z * 16;
+          const double pa = Pv[a * NZ + z], da = Pd[a * NZ + z];
+          // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
+          // plus row 0 weighted by P for x = 2 in the general case)
+          const double wr = x < 2 ? pa : da;
+          const double w0 = (GENERAL && x == 2) ? pa : 0.0;
+          const double L0 = GENERAL ? wr * M[kx * 4 + 0] + w0 * M[0] : 0.0;
+          const double L1 = wr * M[kx * 4 + 1] + (GENERAL ? w0 * M[1] : 0.0);
+          const double L2 = wr * M[kx * 4 + 2] + (GENERAL ? w0 * M[2] : 0.0);
+          const double L3 = wr * M[kx * 4 + 3] + (GENERAL ? w0 * M[3] : 0.0);
+#pragma unroll
+          for (int bb = 0; bb < C::BPER; ++bb) {
+            const int b = bg * C::BPER + bb;
+            if (b < NV) {
+              const double pb = Pv[b * NZ + z], db = Pd[b * NZ + z];
+              h[bb][0] = fma(L1, pb, h[bb][0]);
+              h[bb][1] = fma(L2, pb, h[bb][1]);
+              h[bb][2] = GENERAL ? fma(L0, pb, fma(L3, db, h[bb][2])) : fma(L3, db, h[bb][2]);
+            }
+          }
+        }
+#pragma unroll
+        for (int bb = 0; bb < C::BPER; ++bb) {
+          const int b = bg * C::BPER + bb;
+          if (b < NV) {
+            double* dst = Hb + ((((el * AG + al) * 4 + sl) * NV + b) * 3 + x) * 4;
+            *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
+            dst[2] = h[bb][2];
+          }
+        }
+      }
+      __threadfence_block();
+      named_arrive(kBarFull0 + (chunk & 1), C::NTHREADS);
+      named_sync(kBarProd, C::NPT);  // all producers done with sM before it is rewritten
+    }
+    return;
   }
 
-  // ---- warp task ----
+  // ======================= consumer warps =======================
   const int el_w = warp / C::WPE;
   const int r_w = warp % C::WPE;
-  const int a_w0 = agroup * AG + (r_w / C::NBLK) * WA;  // first Legendre row a of this warp
+  const int al0 = (r_w / C::NBLK) * WA;  // first local a of this warp
   const int nt0 = (r_w % C::NBLK) * NB;
-  double* sG = smem + C::OFF_G + warp * C::G_PER_WARP;
+
+  // Lane constants: B-fragment row kk = ks*4 + lane%4 -> (sl, x); column j = nt*8 + lane/4 -> (t', b).
+  int sl_k[3], x_k[3];
+#pragma unroll
+  for (int ks = 0; ks < 3; ++ks) {
+    const int kk = ks * 4 + (lane & 3);
+    sl_k[ks] = kk / 3;
+    x_k[ks] = kk % 3;
+  }
+  int hoff[NB], xoff[NB];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    const int j = (nt0 + nb) * 8 + (lane >> 2);
+    const int tp = j / NV, b = j - tp * NV;
+    hoff[nb] = b * 12;  // + x*4 at use
+    xoff[nb] = tp * 4;  // + s*NTP*4 at use
+  }
 
   double acc[WA][MT][NB][2];
 #pragma unroll
@@ -158,87 +265,42 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS)
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) acc[wa][mt][nb][0] = acc[wa][mt][nb][1] = 0.0;
 
-  const double* Pv = sY;            // P_a(z)  [NV][NZ]
-  const double* Pd = sY + NV * NZ;  // P'_a(z) [NV][NZ]
-
-  for (int chunk = 0; chunk < C::NCHUNK; ++chunk) {
-    double* Hb = sH + (chunk & 1) * C::H_PER_BUF;
-    __syncthreads();  // M ready (first pass) / previous H buffer reuse is safe
-    // ---- H_xy(s,a,b) for the chunk's 4 triangle points ----
-    for (int i = tid; i < C::H_PER_BUF; i += C::NTHREADS) {
-      // i = (((el*AG + al)*4 + sl)*NV + b)*9 + xy
-      const int xy = i % 9, b = (i / 9) % NV, sl = (i / (9 * NV)) % 4;
-      const int al = (i / (36 * NV)) % AG, el = i / (36 * NV * AG);
-      const int s = chunk * 4 + sl, a = agroup * AG + al;
-      const int x = xy / 3, y = xy % 3;
-      double h = 0.0;
-      if (s < NS) {
-#pragma unroll
-        for (int z = 0; z < NZ; ++z) {
-          const double* M = sM + (el * NQ + z * NS + s) * 16;
-          const double pa = Pv[a * NZ + z], pb = Pv[b * NZ + z];
-          const double da = Pd[a * NZ + z], db = Pd[b * NZ + z];
-          // left factor: sum_{k in x} Y_k(a) M_k. ; right: sum_{l in y} ... Y_l(b)
-          double u[4];
-          if (x < 2) {
-#pragma unroll
-            for (int l = 0; l < 4; ++l) u[l] = pa * M[(x + 1) * 4 + l];
-          } else {
-#pragma unroll
-            for (int l = 0; l < 4; ++l) u[l] = GENERAL ? pa * M[l] + da * M[12 + l] : da * M[12 + l];
-          }
-          if (y < 2) {
-            h += u[y + 1] * pb;
-          } else {
-            h += GENERAL ? u[0] * pb + u[3] * db : u[3] * db;
-          }
-        }
-      }
-      Hb[i] = h;
-    }
-    __syncthreads();
-
-    // ---- G for this warp's (a, n-tile) block, written in B-fragment order ----
-    __syncwarp();
 #pragma unroll 1
-    for (int f = 0; f < WA * NB * 3; ++f) {
-      const int ks = f % 3, nb = (f / 3) % NB, wa = f / (3 * NB);
-      const int kk = ks * 4 + (lane & 3);  // 0..11 within the chunk
-      const int sl = kk / 3, x = kk % 3;
-      const int s = chunk * 4 + sl;
-      const int j = (nt0 + nb) * 8 + (lane >> 2);
-      double g = 0.0;
-      if (s < NS && j < NSH) {
-        const int tp = j / NV, b = j % NV;
-        const int al = a_w0 + wa - agroup * AG;
-        const double* H = Hb + (((el_w * AG + al) * 4 + sl) * NV + b) * 9 + x * 3;
-#pragma unroll
-        for (int yy = 0; yy < 3; ++yy) {
-          const int kx = s * 3 + yy;
-          const double X = sX[((tp >> 3) * KSTEPS + (kx >> 2)) * 32 + (tp & 7) * 4 + (kx & 3)];
-          g += H[yy] * X;
-        }
-      }
-      sG[f * 32 + lane] = g;
-    }
-    __syncwarp();
-
-    // ---- K[t][(a, j)] += X[t][(s,x)] G[(s,x)][(a,j)] on the tensor pipe ----
+  for (int chunk = 0; chunk < NCHUNK; ++chunk) {
+    named_sync(kBarFull0 + (chunk & 1), C::NTHREADS);
+    const double* Hb = sH + (chunk & 1) * C::H_PER_BUF;
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) {
       const int kstep = chunk * 3 + ks;
       double afr[MT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) afr[mt] = sX[(mt * KSTEPS + kstep) * 32 + lane];
+      for (int mt = 0; mt < MT; ++mt) afr[mt] = sXA[(mt * KSTEPS + kstep) * 32 + lane];
+      const int s = chunk * 4 + sl_k[ks];
+      const double* Xs = sXP + s * NTP * 4;
 #pragma unroll
-      for (int wa = 0; wa < WA; ++wa)
+      for (int wa = 0; wa < WA; ++wa) {
+        const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
+        // b for n-tile nb is b_(nb mod R): load each distinct one once
+        double hr[C::RC][3];
+#pragma unroll
+        for (int m = 0; m < C::RC; ++m) {
+          const double2 h01 = *reinterpret_cast<const double2*>(Hs + hoff[m]);
+          hr[m][0] = h01.x;
+          hr[m][1] = h01.y;
+          hr[m][2] = Hs[hoff[m] + 2];
+        }
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
-          const double bfr = sG[((wa * NB + nb) * 3 + ks) * 32 + lane];
+          const double2 x01 = *reinterpret_cast<const double2*>(Xs + xoff[nb]);
+          const double x2 = Xs[xoff[nb] + 2];
+          const double* h = hr[nb % C::R];
+          const double g = fma(h[0], x01.x, fma(h[1], x01.y, h[2] * x2));
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], bfr);
+          for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], g);
         }
+      }
     }
+    if (chunk + 2 < NCHUNK) named_arrive(kBarEmpty0 + (chunk & 1), C::NTHREADS);
   }
 
   // ---- epilogue: fragments -> K rows (t*NV + a), columns j ----
@@ -251,7 +313,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS)
     for (int mt = 0; mt < MT; ++mt) {
       const int t = mt * 8 + (lane >> 2);
       if (t >= NT) continue;
-      const int row = t * NV + a_w0 + wa;
+      const int row = t * NV + agroup * AG + al0 + wa;
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const int j = (nt0 + nb) * 8 + 2 * (lane & 3);

@@ -25,7 +25,7 @@ struct pi_context {
   cudaStream_t stream = nullptr;
   std::vector<double> h_pts, h_w, h_phi;
   double *d_phi = nullptr, *d_pts = nullptr, *d_w = nullptr;
-  double *d_xfrag = nullptr, *d_yline = nullptr, *d_tri = nullptr;
+  double *d_xfrag = nullptr, *d_xplain = nullptr, *d_yline = nullptr, *d_tri = nullptr;
   bool tensor_ok = false;
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
@@ -78,8 +78,8 @@ struct SumFactHost {
   // Builds the X fragment table, Y table and rule coordinates from the
   // caller's rule and shape table; false if the table is not the tensor
   // product the kernel factorises.
-  static bool build(pi_context* ctx, std::vector<double>& xfrag, std::vector<double>& yline,
-                    std::vector<double>& tri) {
+  static bool build(pi_context* ctx, std::vector<double>& xfrag, std::vector<double>& xplain,
+                    std::vector<double>& yline, std::vector<double>& tri) {
     constexpr int NS = C::NS, NZ = C::NZ, NV = C::NV, NT = C::NT, NSH = C::NSH;
     if (ctx->n_q != NS * NZ || ctx->n_shape != NSH) return false;
     const double* pts = ctx->h_pts.data();
@@ -138,6 +138,10 @@ struct SumFactHost {
           if (t < NT && s < NS) v = X[(x * NT + t) * NS + s];
           xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
         }
+    xplain.assign(C::XPLAIN, 0.0);
+    for (int s = 0; s < NS; ++s)
+      for (int t = 0; t < NT; ++t)
+        for (int x = 0; x < 3; ++x) xplain[(static_cast<size_t>(s) * C::NTP + t) * 4 + x] = X[(x * NT + t) * NS + s];
     return true;
   }
 };
@@ -167,9 +171,9 @@ struct AttrOp {
 };
 template <int P>
 struct BuildOp {
-  static void run(pi_context* ctx, std::vector<double>& x, std::vector<double>& y, std::vector<double>& t,
-                  bool& ok) {
-    ok = SumFactHost<P>::build(ctx, x, y, t);
+  static void run(pi_context* ctx, std::vector<double>& x, std::vector<double>& xp, std::vector<double>& y,
+                  std::vector<double>& t, bool& ok) {
+    ok = SumFactHost<P>::build(ctx, x, xp, y, t);
   }
 };
 
@@ -251,12 +255,13 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
 
   if (p >= 2) {
-    std::vector<double> xf, yl, tr;
+    std::vector<double> xf, xp, yl, tr;
     bool ok = false;
-    dispatch_p<BuildOp>(p, ctx, xf, yl, tr, ok);
+    dispatch_p<BuildOp>(p, ctx, xf, xp, yl, tr, ok);
     ctx->tensor_ok = ok;
     if (ok) {
       if ((st = upload(&ctx->d_xfrag, xf, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_xplain, xp, err)) != PI_OK) return fail(st);
       if ((st = upload(&ctx->d_yline, yl, err)) != PI_OK) return fail(st);
       if ((st = upload(&ctx->d_tri, tr, err)) != PI_OK) return fail(st);
       dispatch_p<AttrOp>(p);
@@ -281,6 +286,7 @@ pi_status pi_context_destroy(pi_context* ctx) {
   cudaFree(ctx->d_pts);
   cudaFree(ctx->d_w);
   cudaFree(ctx->d_xfrag);
+  cudaFree(ctx->d_xplain);
   cudaFree(ctx->d_yline);
   cudaFree(ctx->d_tri);
   cudaFree(ctx->d_bad);
@@ -360,7 +366,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
     else
       p1_thread_kernel<false><<<grid, kP1Threads, 0, s>>>(a, t);
   } else {
-    SumFactTables t{ctx->d_xfrag, ctx->d_yline, ctx->d_tri, ctx->d_w};
+    SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
     dispatch_p<LaunchOp>(ctx->p, a, t, general, s);
   }
   PI_CUDA(cudaGetLastError(), "kernel launch");

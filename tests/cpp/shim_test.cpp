@@ -1,0 +1,89 @@
+// C++ drop-in test: the reference's own types and integrate_generic vs the
+// B200 kernels through include/prism_b200_prismint.hpp.  Built against the
+// reference headers + oracle/_ref (tests/cpp/Makefile); run by
+// tests/test_gpu_shim.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "prism_b200_prismint.hpp"
+
+using namespace prismint;
+
+static double rel_frob(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    num += (a[i] - b[i]) * (a[i] - b[i]);
+    den += a[i] * a[i];
+  }
+  return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+int main() {
+  int failures = 0;
+  const auto mesh = generate_box_mesh(3, 2, 2, 0.2, 31);
+  for (int p = 1; p <= 7; ++p) {
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    CoefficientTensor lap = CoefficientTensor::zeros(1);
+    for (int d = 1; d <= 3; ++d) lap.set(0, 0, d, d, 1.0);
+    const auto got = prism_b200::run_batch(p, mesh, lap);
+    const QuadCoefficients qc = expand_coefficients(lap, rule);
+    double worst = 0;
+    for (size_t e = 0; e < mesh.size(); e += (p >= 6 ? 11 : 1)) {
+      const ElementStiffness ref = integrate_generic(mesh[e], qc, shapes, rule);
+      worst = std::max(worst, rel_frob(ref.data, got[e].data));
+    }
+    std::printf("p=%d run_batch vs integrate_generic: %.3e\n", p, worst);
+    if (!(worst <= 1e-12)) ++failures;
+  }
+  // per-element coefficient tensors
+  {
+    const int p = 3;
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    std::vector<CoefficientTensor> cs;
+    for (size_t e = 0; e < mesh.size(); ++e) {
+      CoefficientTensor c = CoefficientTensor::zeros(1);
+      for (int d = 1; d <= 3; ++d) c.set(0, 0, d, d, 1.0 + 0.1 * e);
+      c.set(0, 0, 0, 1, 0.3);
+      c.set(0, 0, 0, 0, 0.05 * e);
+      cs.push_back(c);
+    }
+    const auto got = prism_b200::integrate_batch(mesh, cs, shapes, rule);
+    double worst = 0;
+    for (size_t e = 0; e < mesh.size(); ++e) {
+      const ElementStiffness ref = integrate_generic(mesh[e], expand_coefficients(cs[e], rule), shapes, rule);
+      worst = std::max(worst, rel_frob(ref.data, got[e].data));
+    }
+    std::printf("per-element coefficients p=3: %.3e\n", worst);
+    if (!(worst <= 1e-12)) ++failures;
+  }
+  // error mapping: inverted element with batch offset, table mismatch
+  {
+    auto bad = generate_box_mesh(2, 2, 1, 0.0);
+    std::swap(bad[6].vertices[0], bad[6].vertices[1]);
+    const QuadratureRule rule = prism_quadrature(2);
+    const ShapeTable shapes = tabulate_shapes(2, rule);
+    CoefficientTensor lap = CoefficientTensor::zeros(1);
+    for (int d = 1; d <= 3; ++d) lap.set(0, 0, d, d, 1.0);
+    try {
+      prism_b200::Context ctx(shapes, rule);
+      (void)ctx.integrate(bad, std::span<const CoefficientTensor>(&lap, 1), 100);
+      std::printf("expected InvertedElementError\n");
+      ++failures;
+    } catch (const InvertedElementError& e) {
+      std::printf("InvertedElementError element=%lld det=%g\n", (long long)e.element(), e.det());
+      if (e.element() != 106) ++failures;
+    }
+    try {
+      const QuadratureRule r3 = prism_quadrature(3);
+      prism_b200::Context ctx(shapes, r3);
+      ++failures;
+    } catch (const ConfigError&) {
+      std::printf("ConfigError on table mismatch: ok\n");
+    }
+  }
+  std::printf(failures ? "FAILED %d\n" : "ALL OK\n", failures);
+  return failures ? 1 : 0;
+}
