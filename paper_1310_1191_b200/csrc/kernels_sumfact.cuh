@@ -28,7 +28,12 @@
 
 namespace pib {
 
-template <int P>
+// Column order of a K row block inside the GEMM ("n-tiles" of 8 columns):
+//  natural: n-tile nt = columns j = 8 nt .. 8 nt + 7, j = t'*(p+1) + b;
+//  t'-major (TMAJOR): n-tile (g, b) = columns t' = 8g .. 8g+7 at fixed b, so
+//  a lane's X values are shared by every b-tile and H is warp-uniform per
+//  tile (the better order when p+1 does not divide 8).
+template <int P, bool TMAJOR>
 struct SumFactShape {
   static constexpr int NV = P + 1;                    // Legendre modes / GL points
   static constexpr int NZ = P + 1;
@@ -37,9 +42,9 @@ struct SumFactShape {
   static constexpr int NSP = (NS + 3) / 4 * 4;        // padded to whole chunks
   static constexpr int NSH = NT * NV;
   static constexpr int NQ = NS * NZ;
-  static constexpr int MT = (NT + 7) / 8;             // m-tiles of the X operand
-  static constexpr int NTILE = (NSH + 7) / 8;         // n-tiles of one K row block
-  static constexpr int NTP = (NTILE * 8 + NV - 1) / NV;  // t' range covered by padded columns
+  static constexpr int MT = (NT + 7) / 8;             // m-tiles of the X operand (rows t)
+  static constexpr int NTILE = TMAJOR ? MT * NV : (NSH + 7) / 8;
+  static constexpr int NTP = TMAJOR ? MT * 8 : (NTILE * 8 + NV - 1) / NV;  // t' rows of the X table
   static constexpr int KSTEPS = 3 * NSP / 4;          // k4-steps over (s, x)
   static constexpr int NCHUNK = NSP / 4;              // 4 triangle points per chunk
   static constexpr int XFRAG = MT * KSTEPS * 32;      // doubles in the A-fragment table
@@ -48,22 +53,44 @@ struct SumFactShape {
 
 // Launch shape: EPC elements x AG Legendre rows `a` per CTA; each consumer
 // warp owns WA rows a x NB n-tiles x all MT m-tiles (WA*NB*MT fragments);
-// NPW producer warps.
+// NPW producer warps.  TMAJOR warps own NG t'-groups x NBB b values (NB = NG*NBB).
 template <int P>
 struct SumFactLaunch;
-template <> struct SumFactLaunch<2> { static constexpr int EPC = 8, AG = 3, WA = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 2; };
-template <> struct SumFactLaunch<3> { static constexpr int EPC = 4, AG = 4, WA = 2, NB = 5, NPW = 4, BSPLIT = 1, MINB = 1; };
-template <> struct SumFactLaunch<4> { static constexpr int EPC = 1, AG = 5, WA = 1, NB = 10, NPW = 2, BSPLIT = 1, MINB = 2; };
-template <> struct SumFactLaunch<5> { static constexpr int EPC = 1, AG = 3, WA = 1, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1; };
-template <> struct SumFactLaunch<6> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1; };
-template <> struct SumFactLaunch<7> { static constexpr int EPC = 1, AG = 1, WA = 1, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1; };
+template <> struct SumFactLaunch<2> {
+  static constexpr bool TMAJOR = true;
+  static constexpr int EPC = 8, AG = 3, WA = 3, NG = 1, NBB = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 1;
+};
+template <> struct SumFactLaunch<3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 4, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 4, BSPLIT = 1, MINB = 1;
+};
+template <> struct SumFactLaunch<4> {
+  static constexpr bool TMAJOR = true;
+  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 2, BSPLIT = 1, MINB = 2;
+};
+template <> struct SumFactLaunch<5> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1;
+};
+template <> struct SumFactLaunch<6> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1;
+};
+template <> struct SumFactLaunch<7> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1;
+};
 
 template <int P>
-struct SumFactConfig : SumFactShape<P>, SumFactLaunch<P> {
-  using S = SumFactShape<P>;
+struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<P> {
+  using S = SumFactShape<P, SumFactLaunch<P>::TMAJOR>;
   using L = SumFactLaunch<P>;
   static constexpr int NBLK = S::NTILE / L::NB;
   static constexpr int WPE = (L::AG / L::WA) * NBLK;   // consumer warps per element
+  // t'-major warps own whole K rows (all t'-groups, all b), so they stage
+  // and store their rows without CTA-level synchronisation.
+  static_assert(!L::TMAJOR || (L::NB == L::NG * L::NBB && L::NG == S::MT && L::NBB == S::NV),
+                "t'-major warp tiling");
   static constexpr int NCW = L::EPC * WPE;
   static constexpr int NWARPS = NCW + L::NPW;
   static constexpr int NTHREADS = 32 * NWARPS;
@@ -89,7 +116,10 @@ struct SumFactConfig : SumFactShape<P>, SumFactLaunch<P> {
   static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
   static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
-  static constexpr int SMEM_DOUBLES = OFF_W + S::NQ;
+  // t'-major epilogue: each consumer warp stages its WA*NT K rows
+  static constexpr int STAGE_PER_WARP = L::TMAJOR ? (L::WA * S::NT * S::NSH + 1) / 2 * 2 : 0;
+  static constexpr int OFF_STAGE = (OFF_W + S::NQ + 1) / 2 * 2;
+  static constexpr int SMEM_DOUBLES = OFF_STAGE + NCW * STAGE_PER_WARP;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
 };
 
@@ -108,7 +138,7 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProd = 5;
+constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProd = 5, kBarCons = 6;
 
 template <int P, bool GENERAL>
 __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::MINB)
@@ -129,107 +159,116 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   double* sW = smem + C::OFF_W;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t egroup = blockIdx.x / C::NAG;
-  const int agroup = blockIdx.x % C::NAG;
-  const int64_t e0 = egroup * EPC;
 
-  // ---- stage per-p tables and per-element inputs (all warps) ----
+  // ---- per-p tables: staged once per (persistent) CTA ----
   for (int i = tid; i < C::XFRAG; i += C::NTHREADS) sXA[i] = tab.xfrag[i];
   for (int i = tid; i < C::XPLAIN; i += C::NTHREADS) sXP[i] = tab.xplain[i];
   for (int i = tid; i < 2 * NV * NZ + NZ; i += C::NTHREADS) sY[i] = tab.yline[i];
   for (int i = tid; i < 2 * NS; i += C::NTHREADS) sTri[i] = tab.tri[i];
   for (int i = tid; i < NQ; i += C::NTHREADS) sW[i] = tab.w[i];
-  for (int i = tid; i < EPC * 18; i += C::NTHREADS) {
-    const int el = i / 18, c = i % 18;
-    const int64_t e = e0 + el;
-    const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;  // pad with a valid element
-    sGeom[i] = args.geom[c * args.geom_ld + ec];
-  }
-  if (GENERAL) {
-    for (int i = tid; i < EPC * 16; i += C::NTHREADS) {
-      const int el = i / 16, c = i % 16;
-      const int64_t e = e0 + el;
-      const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;
-      sC[i] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
-    }
-  }
   __syncthreads();
 
   const double* Pv = sY;            // P_a(z)  [NV][NZ]
   const double* Pd = sY + NV * NZ;  // P'_a(z) [NV][NZ]
 
+  // Work items: (element group, a-group); this CTA takes items blockIdx.x + k*gridDim.x.
+  const int64_t n_items = (args.n_elem + EPC - 1) / EPC * C::NAG;
+  const int64_t my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total_chunks = my_items * NCHUNK;
+
   if (warp >= C::NCW) {
     // ======================= producer warps =======================
     const int ptid = tid - 32 * C::NCW;
-    for (int chunk = 0; chunk < NCHUNK; ++chunk) {
-      // (1) M for the chunk's points: (el, sl, z)
-      for (int i = ptid; i < EPC * 4 * NZ; i += C::NPT) {
-        const int z = i % NZ, sl = (i / NZ) % 4, el = i / (4 * NZ);
-        const int s = chunk * 4 + sl;
-        double M[16];
-        if (s < NS) {
-          double inv[3][3];
-          const double det = prism_jacobian(sGeom + 18 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], inv);
+    int64_t gc = 0;  // chunk counter across items: selects the H buffer
+    for (int64_t it = 0; it < my_items; ++it) {
+      const int64_t w = blockIdx.x + it * gridDim.x;
+      const int64_t e0 = (w / C::NAG) * EPC;
+      const int agroup = static_cast<int>(w % C::NAG);
+      for (int i = ptid; i < EPC * 18; i += C::NPT) {
+        const int el = i / 18, c = i % 18;
+        const int64_t e = e0 + el;
+        const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;  // pad with a valid element
+        sGeom[i] = args.geom[c * args.geom_ld + ec];
+      }
+      if (GENERAL) {
+        for (int i = ptid; i < EPC * 16; i += C::NPT) {
+          const int el = i / 16, c = i % 16;
           const int64_t e = e0 + el;
-          if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
-          coefficient_block<GENERAL>(inv, det * sW[z * NS + s], sC + 16 * el, M);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) M[k] = 0.0;
+          const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;
+          sC[i] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
         }
-        double2* dst = reinterpret_cast<double2*>(sM + i * 16);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) dst[k] = make_double2(M[2 * k], M[2 * k + 1]);
       }
       named_sync(kBarProd, C::NPT);
-      if (chunk >= 2) named_sync(kBarEmpty0 + (chunk & 1), C::NTHREADS);  // consumers released this buffer
-      double* Hb = sH + (chunk & 1) * C::H_PER_BUF;
-      // (2) H_x,y(s,a,b), y = 0..2: items (el, al, sl, x, b-group), b looped
-      for (int i = ptid; i < EPC * AG * 4 * 3 * C::BSPLIT; i += C::NPT) {
-        const int bg = i % C::BSPLIT, x = (i / C::BSPLIT) % 3, sl = (i / (3 * C::BSPLIT)) % 4;
-        const int al = (i / (12 * C::BSPLIT)) % AG, el = i / (12 * C::BSPLIT * AG);
-        const int a = agroup * AG + al;
-        const int kx = x < 2 ? x + 1 : 3;
-        double h[C::BPER][3];
+      for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
+        // (1) M for the chunk's points: (el, sl, z)
+        for (int i = ptid; i < EPC * 4 * NZ; i += C::NPT) {
+          const int z = i % NZ, sl = (i / NZ) % 4, el = i / (4 * NZ);
+          const int s = chunk * 4 + sl;
+          double M[16];
+          if (s < NS) {
+            double inv[3][3];
+            const double det = prism_jacobian(sGeom + 18 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], inv);
+            const int64_t e = e0 + el;
+            if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
+            coefficient_block<GENERAL>(inv, det * sW[z * NS + s], sC + 16 * el, M);
+          } else {
 #pragma unroll
-        for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
-        const double* Mp = sM + (el * 4 + sl) * NZ * 16;
+            for (int k = 0; k < 16; ++k) M[k] = 0.0;
+          }
+          double2* dst = reinterpret_cast<double2*>(sM + i * 16);
 #pragma unroll
-        for (int z = 0; z < NZ; ++z) {
-          const double* M = Mp + z * 16;
-          const double pa = Pv[a * NZ + z], da = Pd[a * NZ + z];
-          // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
-          // plus row 0 weighted by P for x = 2 in the general case)
-          const double wr = x < 2 ? pa : da;
-          const double w0 = (GENERAL && x == 2) ? pa : 0.0;
-          const double L0 = GENERAL ? wr * M[kx * 4 + 0] + w0 * M[0] : 0.0;
-          const double L1 = wr * M[kx * 4 + 1] + (GENERAL ? w0 * M[1] : 0.0);
-          const double L2 = wr * M[kx * 4 + 2] + (GENERAL ? w0 * M[2] : 0.0);
-          const double L3 = wr * M[kx * 4 + 3] + (GENERAL ? w0 * M[3] : 0.0);
+          for (int k = 0; k < 8; ++k) dst[k] = make_double2(M[2 * k], M[2 * k + 1]);
+        }
+        named_sync(kBarProd, C::NPT);
+        if (gc >= 2) named_sync(kBarEmpty0 + (gc & 1), C::NTHREADS);  // consumers released this buffer
+        double* Hb = sH + (gc & 1) * C::H_PER_BUF;
+        // (2) H_x,y(s,a,b), y = 0..2: items (el, al, sl, x, b-group), b looped
+        for (int i = ptid; i < EPC * AG * 4 * 3 * C::BSPLIT; i += C::NPT) {
+          const int bg = i % C::BSPLIT, x = (i / C::BSPLIT) % 3, sl = (i / (3 * C::BSPLIT)) % 4;
+          const int al = (i / (12 * C::BSPLIT)) % AG, el = i / (12 * C::BSPLIT * AG);
+          const int a = agroup * AG + al;
+          const int kx = x < 2 ? x + 1 : 3;
+          double h[C::BPER][3];
+#pragma unroll
+          for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
+          const double* Mp = sM + (el * 4 + sl) * NZ * 16;
+#pragma unroll
+          for (int z = 0; z < NZ; ++z) {
+            const double* M = Mp + z * 16;
+            const double pa = Pv[a * NZ + z], da = Pd[a * NZ + z];
+            // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
+            // plus row 0 weighted by P for x = 2 in the general case)
+            const double wr = x < 2 ? pa : da;
+            const double w0 = (GENERAL && x == 2) ? pa : 0.0;
+            const double L0 = GENERAL ? wr * M[kx * 4 + 0] + w0 * M[0] : 0.0;
+            const double L1 = wr * M[kx * 4 + 1] + (GENERAL ? w0 * M[1] : 0.0);
+            const double L2 = wr * M[kx * 4 + 2] + (GENERAL ? w0 * M[2] : 0.0);
+            const double L3 = wr * M[kx * 4 + 3] + (GENERAL ? w0 * M[3] : 0.0);
+#pragma unroll
+            for (int bb = 0; bb < C::BPER; ++bb) {
+              const int b = bg * C::BPER + bb;
+              if (b < NV) {
+                const double pb = Pv[b * NZ + z], db = Pd[b * NZ + z];
+                h[bb][0] = fma(L1, pb, h[bb][0]);
+                h[bb][1] = fma(L2, pb, h[bb][1]);
+                h[bb][2] = GENERAL ? fma(L0, pb, fma(L3, db, h[bb][2])) : fma(L3, db, h[bb][2]);
+              }
+            }
+          }
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) {
             const int b = bg * C::BPER + bb;
             if (b < NV) {
-              const double pb = Pv[b * NZ + z], db = Pd[b * NZ + z];
-              h[bb][0] = fma(L1, pb, h[bb][0]);
-              h[bb][1] = fma(L2, pb, h[bb][1]);
-              h[bb][2] = GENERAL ? fma(L0, pb, fma(L3, db, h[bb][2])) : fma(L3, db, h[bb][2]);
+              double* dst = Hb + ((((el * AG + al) * 4 + sl) * NV + b) * 3 + x) * 4;
+              *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
+              dst[2] = h[bb][2];
             }
           }
         }
-#pragma unroll
-        for (int bb = 0; bb < C::BPER; ++bb) {
-          const int b = bg * C::BPER + bb;
-          if (b < NV) {
-            double* dst = Hb + ((((el * AG + al) * 4 + sl) * NV + b) * 3 + x) * 4;
-            *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
-            dst[2] = h[bb][2];
-          }
-        }
+        __threadfence_block();
+        named_arrive(kBarFull0 + (gc & 1), C::NTHREADS);
+        named_sync(kBarProd, C::NPT);  // all producers done with sM / sGeom before they are rewritten
       }
-      __threadfence_block();
-      named_arrive(kBarFull0 + (chunk & 1), C::NTHREADS);
-      named_sync(kBarProd, C::NPT);  // all producers done with sM before it is rewritten
     }
     return;
   }
@@ -238,9 +277,11 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   const int el_w = warp / C::WPE;
   const int r_w = warp % C::WPE;
   const int al0 = (r_w / C::NBLK) * WA;  // first local a of this warp
-  const int nt0 = (r_w % C::NBLK) * NB;
+  const int nblk = r_w % C::NBLK;
+  const int cpos = lane >> 2;            // B-fragment column within an n-tile
+  const int64_t kk_elem = static_cast<int64_t>(NSH) * NSH;
 
-  // Lane constants: B-fragment row kk = ks*4 + lane%4 -> (sl, x); column j = nt*8 + lane/4 -> (t', b).
+  // B-fragment row kk = ks*4 + lane%4 -> (sl, x) for the three k-steps of a chunk
   int sl_k[3], x_k[3];
 #pragma unroll
   for (int ks = 0; ks < 3; ++ks) {
@@ -249,89 +290,159 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     x_k[ks] = kk % 3;
   }
   int hoff[NB], xoff[NB];
+  if constexpr (!C::TMAJOR) {
 #pragma unroll
-  for (int nb = 0; nb < NB; ++nb) {
-    const int j = (nt0 + nb) * 8 + (lane >> 2);
-    const int tp = j / NV, b = j - tp * NV;
-    hoff[nb] = b * 12;  // + x*4 at use
-    xoff[nb] = tp * 4;  // + s*NTP*4 at use
+    for (int nb = 0; nb < NB; ++nb) {
+      const int j = (nblk * NB + nb) * 8 + cpos;
+      const int tp = j / NV, b = j - tp * NV;
+      hoff[nb] = b * 12;  // + x*4 at use
+      xoff[nb] = tp * 4;  // + s*NTP*4 at use
+    }
   }
 
-  double acc[WA][MT][NB][2];
+  int64_t gc = 0;
+  for (int64_t it = 0; it < my_items; ++it) {
+    const int64_t w = blockIdx.x + it * gridDim.x;
+    const int64_t e = (w / C::NAG) * EPC + el_w;
+    const int agroup = static_cast<int>(w % C::NAG);
+
+    double acc[WA][MT][NB][2];
 #pragma unroll
-  for (int wa = 0; wa < WA; ++wa)
+    for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-      for (int nb = 0; nb < NB; ++nb) acc[wa][mt][nb][0] = acc[wa][mt][nb][1] = 0.0;
+        for (int nb = 0; nb < NB; ++nb) acc[wa][mt][nb][0] = acc[wa][mt][nb][1] = 0.0;
 
 #pragma unroll 1
-  for (int chunk = 0; chunk < NCHUNK; ++chunk) {
-    named_sync(kBarFull0 + (chunk & 1), C::NTHREADS);
-    const double* Hb = sH + (chunk & 1) * C::H_PER_BUF;
+    for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
+      named_sync(kBarFull0 + (gc & 1), C::NTHREADS);
+      const double* Hb = sH + (gc & 1) * C::H_PER_BUF;
 #pragma unroll
-    for (int ks = 0; ks < 3; ++ks) {
-      const int kstep = chunk * 3 + ks;
-      double afr[MT];
+      for (int ks = 0; ks < 3; ++ks) {
+        const int kstep = chunk * 3 + ks;
+        double afr[MT];
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) afr[mt] = sXA[(mt * KSTEPS + kstep) * 32 + lane];
-      const int s = chunk * 4 + sl_k[ks];
-      const double* Xs = sXP + s * NTP * 4;
+        for (int mt = 0; mt < MT; ++mt) afr[mt] = sXA[(mt * KSTEPS + kstep) * 32 + lane];
+        const int s = chunk * 4 + sl_k[ks];
+        if constexpr (C::TMAJOR) {
+          // n-tile (g, b): columns t' = 8g + cpos at fixed b; lane's X shared by all b
+          double xv[MT][3];
 #pragma unroll
-      for (int wa = 0; wa < WA; ++wa) {
-        const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
-        // b for n-tile nb is b_(nb mod R): load each distinct one once
-        double hr[C::RC][3];
+          for (int g = 0; g < MT; ++g) {
+            const double* xp = sXP + (s * NTP + g * 8 + cpos) * 4;
+            const double2 x01 = *reinterpret_cast<const double2*>(xp);
+            xv[g][0] = x01.x;
+            xv[g][1] = x01.y;
+            xv[g][2] = xp[2];
+          }
 #pragma unroll
-        for (int m = 0; m < C::RC; ++m) {
-          const double2 h01 = *reinterpret_cast<const double2*>(Hs + hoff[m]);
-          hr[m][0] = h01.x;
-          hr[m][1] = h01.y;
-          hr[m][2] = Hs[hoff[m] + 2];
-        }
+          for (int wa = 0; wa < WA; ++wa) {
+            const double* Hs = Hb + ((((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 3 + x_k[ks]) * 4;
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) {
-          const double2 x01 = *reinterpret_cast<const double2*>(Xs + xoff[nb]);
-          const double x2 = Xs[xoff[nb] + 2];
-          const double* h = hr[nb % C::R];
-          const double g = fma(h[0], x01.x, fma(h[1], x01.y, h[2] * x2));
+            for (int b = 0; b < NV; ++b) {
+              const double2 h01 = *reinterpret_cast<const double2*>(Hs + b * 12);
+              const double h2 = Hs[b * 12 + 2];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], g);
-        }
-      }
-    }
-    if (chunk + 2 < NCHUNK) named_arrive(kBarEmpty0 + (chunk & 1), C::NTHREADS);
-  }
-
-  // ---- epilogue: fragments -> K rows (t*NV + a), columns j ----
-  const int64_t e = e0 + el_w;
-  if (e >= args.n_elem) return;
-  const int64_t kk_elem = static_cast<int64_t>(NSH) * NSH;
+              for (int g = 0; g < MT; ++g) {
+                const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
 #pragma unroll
-  for (int wa = 0; wa < WA; ++wa)
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int t = mt * 8 + (lane >> 2);
-      if (t >= NT) continue;
-      const int row = t * NV + agroup * AG + al0 + wa;
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb) {
-        const int j = (nt0 + nb) * 8 + 2 * (lane & 3);
-        if (args.out_layout == PI_OUT_CANONICAL) {
-          double* dst = args.out + e * kk_elem + static_cast<int64_t>(row) * NSH + j;
-          if ((NSH % 2 == 0) && j + 1 < NSH) {
-            *reinterpret_cast<double2*>(dst) = make_double2(acc[wa][mt][nb][0], acc[wa][mt][nb][1]);
-          } else {
-            if (j < NSH) dst[0] = acc[wa][mt][nb][0];
-            if (j + 1 < NSH) dst[1] = acc[wa][mt][nb][1];
+                for (int mt = 0; mt < MT; ++mt)
+                  dmma_8x8x4(acc[wa][mt][g * NV + b][0], acc[wa][mt][g * NV + b][1], afr[mt], gv);
+              }
+            }
           }
         } else {
-          const int64_t base = static_cast<int64_t>(row) * NSH + j;
-          if (j < NSH) args.out[base * args.ld_out + e] = acc[wa][mt][nb][0];
-          if (j + 1 < NSH) args.out[(base + 1) * args.ld_out + e] = acc[wa][mt][nb][1];
+          const double* Xs = sXP + s * NTP * 4;
+#pragma unroll
+          for (int wa = 0; wa < WA; ++wa) {
+            const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
+            // b for n-tile nb is b_(nb mod R): load each distinct one once
+            double hr[C::RC][3];
+#pragma unroll
+            for (int m = 0; m < C::RC; ++m) {
+              const double2 h01 = *reinterpret_cast<const double2*>(Hs + hoff[m]);
+              hr[m][0] = h01.x;
+              hr[m][1] = h01.y;
+              hr[m][2] = Hs[hoff[m] + 2];
+            }
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+              const double2 x01 = *reinterpret_cast<const double2*>(Xs + xoff[nb]);
+              const double x2 = Xs[xoff[nb] + 2];
+              const double* h = hr[nb % C::R];
+              const double gv = fma(h[0], x01.x, fma(h[1], x01.y, h[2] * x2));
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], gv);
+            }
+          }
         }
       }
+      if (gc + 2 < total_chunks) named_arrive(kBarEmpty0 + (gc & 1), C::NTHREADS);
     }
+
+    // ---- epilogue (overlaps the producers' next item) ----
+    if (e >= args.n_elem) continue;
+    if constexpr (C::TMAJOR) {
+      // warp-private staging of its WA*NT full K rows, then row-wise coalesced stores
+      double* st = smem + C::OFF_STAGE + warp * C::STAGE_PER_WARP;
+#pragma unroll
+      for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t = mt * 8 + (lane >> 2);
+#pragma unroll
+          for (int g = 0; g < MT; ++g)
+#pragma unroll
+            for (int b = 0; b < NV; ++b)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int tp = g * 8 + 2 * (lane & 3) + h;
+                if (t < NT && tp < NT) st[(wa * NT + t) * NSH + tp * NV + b] = acc[wa][mt][g * NV + b][h];
+              }
+        }
+      __syncwarp();
+#pragma unroll 1
+      for (int r = 0; r < WA * NT; ++r) {
+        const int wa = r / NT, t = r % NT;
+        const int64_t row = t * NV + agroup * AG + al0 + wa;
+        const double* src = st + r * NSH;
+        if (args.out_layout == PI_OUT_CANONICAL) {
+          double* dst = args.out + e * kk_elem + row * NSH;
+          for (int j = lane; j < NSH; j += 32) dst[j] = src[j];
+        } else {
+          for (int j = lane; j < NSH; j += 32) args.out[(row * NSH + j) * args.ld_out + e] = src[j];
+        }
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t = mt * 8 + (lane >> 2);
+          if (t >= NT) continue;
+          const int row = t * NV + agroup * AG + al0 + wa;
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) {
+            const int j = (nblk * NB + nb) * 8 + 2 * (lane & 3);
+            if (args.out_layout == PI_OUT_CANONICAL) {
+              double* dst = args.out + e * kk_elem + static_cast<int64_t>(row) * NSH + j;
+              if ((NSH % 2 == 0) && j + 1 < NSH) {
+                *reinterpret_cast<double2*>(dst) = make_double2(acc[wa][mt][nb][0], acc[wa][mt][nb][1]);
+              } else {
+                if (j < NSH) dst[0] = acc[wa][mt][nb][0];
+                if (j + 1 < NSH) dst[1] = acc[wa][mt][nb][1];
+              }
+            } else {
+              const int64_t base = static_cast<int64_t>(row) * NSH + j;
+              if (j < NSH) args.out[base * args.ld_out + e] = acc[wa][mt][nb][0];
+              if (j + 1 < NSH) args.out[(base + 1) * args.ld_out + e] = acc[wa][mt][nb][1];
+            }
+          }
+        }
+    }
+  }
 }
 
 }  // namespace pib

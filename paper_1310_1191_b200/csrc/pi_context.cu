@@ -67,9 +67,26 @@ struct SumFactHost {
     cudaFuncSetAttribute(sumfact_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM_BYTES));
   }
+  // Persistent grid: as many CTAs as fit on the device at once (queried per
+  // instantiation), each looping over (element group, a-group) work items.
+  static int resident_ctas(bool general) {
+    static int cached[2] = {0, 0};
+    int& c = cached[general ? 1 : 0];
+    if (c == 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (general)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, true>, C::NTHREADS, C::SMEM_BYTES);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, false>, C::NTHREADS, C::SMEM_BYTES);
+      c = std::max(1, sms * std::max(1, per_sm));
+    }
+    return c;
+  }
   static void launch(const LaunchArgs& a, const SumFactTables& t, bool general, cudaStream_t s) {
-    const int64_t groups = (a.n_elem + C::EPC - 1) / C::EPC;
-    const dim3 grid(static_cast<unsigned>(groups * C::NAG));
+    const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NAG;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas(general))));
     if (general)
       sumfact_kernel<P, true><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
     else
