@@ -169,7 +169,7 @@ def run_reference_arm(args, ps, ws, rank):
     from oracle_lib import Reference, laplace_tensor
 
     ref = Reference()
-    n_p = {p: max(1, int(rates[p] * budget / len(ps))) for p in ps}
+    n_p = {p: min(len(mesh), max(1, int(rates[p] * budget / len(ps)))) for p in ps}
 
     def one_step(acc):
         for p in ps:

@@ -66,7 +66,7 @@ template <> struct SumFactLaunch<3> {
 };
 template <> struct SumFactLaunch<4> {
   static constexpr bool TMAJOR = true;
-  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 2, BSPLIT = 1, MINB = 2;
+  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 3, BSPLIT = 1, MINB = 2;
 };
 template <> struct SumFactLaunch<5> {
   static constexpr bool TMAJOR = false;
@@ -105,12 +105,13 @@ struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<
   static_assert(S::NTILE % L::NB == 0, "n-tiles must split evenly");
   // H for one chunk: [EPC][AG][4 s][NV b][3 x][4 y (padded)]
   static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NV * 12;
+  static constexpr int NBUF = 3;  // H ring depth (producers run up to NBUF chunks ahead)
   static constexpr int M_PER_CHUNK = L::EPC * 4 * S::NZ * 16;
   // shared memory layout (doubles; every block 16-byte aligned)
   static constexpr int OFF_XA = 0;
   static constexpr int OFF_XP = OFF_XA + S::XFRAG;
   static constexpr int OFF_H = OFF_XP + S::XPLAIN;
-  static constexpr int OFF_M = OFF_H + 2 * H_PER_BUF;
+  static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
   static constexpr int OFF_GEOM = OFF_M + M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + L::EPC * 18;
   static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
@@ -138,7 +139,10 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProd = 5, kBarCons = 6;
+constexpr int kBarFull0 = 1, kBarEmpty0 = 4, kBarProd = 7, kBarCons = 8;  // FULL/EMPTY: 3 ids each
+
+// Release fence for the shared-memory hand-off before bar.arrive (MEMBAR.ALL.CTA).
+__device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
 
 template <int P, bool GENERAL>
 __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::MINB)
@@ -220,8 +224,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           for (int k = 0; k < 8; ++k) dst[k] = make_double2(M[2 * k], M[2 * k + 1]);
         }
         named_sync(kBarProd, C::NPT);
-        if (gc >= 2) named_sync(kBarEmpty0 + (gc & 1), C::NTHREADS);  // consumers released this buffer
-        double* Hb = sH + (gc & 1) * C::H_PER_BUF;
+        const int buf = static_cast<int>(gc % C::NBUF);
+        if (gc >= C::NBUF) named_sync(kBarEmpty0 + buf, C::NTHREADS);  // consumers released this buffer
+        double* Hb = sH + buf * C::H_PER_BUF;
         // (2) H_x,y(s,a,b), y = 0..2: items (el, al, sl, x, b-group), b looped
         for (int i = ptid; i < EPC * AG * 4 * 3 * C::BSPLIT; i += C::NPT) {
           const int bg = i % C::BSPLIT, x = (i / C::BSPLIT) % 3, sl = (i / (3 * C::BSPLIT)) % 4;
@@ -265,8 +270,8 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
             }
           }
         }
-        __threadfence_block();
-        named_arrive(kBarFull0 + (gc & 1), C::NTHREADS);
+        smem_release();
+        named_arrive(kBarFull0 + buf, C::NTHREADS);
         named_sync(kBarProd, C::NPT);  // all producers done with sM / sGeom before they are rewritten
       }
     }
@@ -316,14 +321,18 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 
 #pragma unroll 1
     for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
-      named_sync(kBarFull0 + (gc & 1), C::NTHREADS);
-      const double* Hb = sH + (gc & 1) * C::H_PER_BUF;
+      // A fragments of the chunk (static table) before waiting for H
+      double afr3[3][MT];
+#pragma unroll
+      for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) afr3[ks][mt] = sXA[(mt * KSTEPS + chunk * 3 + ks) * 32 + lane];
+      const int buf = static_cast<int>(gc % C::NBUF);
+      named_sync(kBarFull0 + buf, C::NTHREADS);
+      const double* Hb = sH + buf * C::H_PER_BUF;
 #pragma unroll
       for (int ks = 0; ks < 3; ++ks) {
-        const int kstep = chunk * 3 + ks;
-        double afr[MT];
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) afr[mt] = sXA[(mt * KSTEPS + kstep) * 32 + lane];
+        const double* afr = afr3[ks];
         const int s = chunk * 4 + sl_k[ks];
         if constexpr (C::TMAJOR) {
           // n-tile (g, b): columns t' = 8g + cpos at fixed b; lane's X shared by all b
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           }
         }
       }
-      if (gc + 2 < total_chunks) named_arrive(kBarEmpty0 + (gc & 1), C::NTHREADS);
+      if (gc + C::NBUF < total_chunks) named_arrive(kBarEmpty0 + buf, C::NTHREADS);
     }
 
     // ---- epilogue (overlaps the producers' next item) ----
@@ -402,16 +411,21 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
               }
         }
       __syncwarp();
-#pragma unroll 1
-      for (int r = 0; r < WA * NT; ++r) {
-        const int wa = r / NT, t = r % NT;
-        const int64_t row = t * NV + agroup * AG + al0 + wa;
-        const double* src = st + r * NSH;
-        if (args.out_layout == PI_OUT_CANONICAL) {
-          double* dst = args.out + e * kk_elem + row * NSH;
-          for (int j = lane; j < NSH; j += 32) dst[j] = src[j];
-        } else {
-          for (int j = lane; j < NSH; j += 32) args.out[(row * NSH + j) * args.ld_out + e] = src[j];
+      const int64_t row0 = agroup * AG + al0;  // row of (t = 0, wa = 0); row(t, wa) = row0 + t*NV + wa
+      if (args.out_layout == PI_OUT_CANONICAL) {
+        double* dst = args.out + e * kk_elem + row0 * NSH;
+#pragma unroll
+        for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+          for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int j0 = 0; j0 < NSH; j0 += 32)
+              if (j0 + lane < NSH) dst[(t * NV + wa) * NSH + j0 + lane] = st[(wa * NT + t) * NSH + j0 + lane];
+      } else {
+        for (int r = 0; r < WA * NT; ++r) {
+          const int wa = r / NT, t = r % NT;
+          const int64_t row = row0 + t * NV + wa;
+          for (int j = lane; j < NSH; j += 32) args.out[(row * NSH + j) * args.ld_out + e] = st[r * NSH + j];
         }
       }
       __syncwarp();
