@@ -144,10 +144,14 @@ constexpr int kBarFull0 = 1, kBarEmpty0 = 4, kBarProd = 7, kBarCons = 8;  // FUL
 // Release fence for the shared-memory hand-off before bar.arrive (MEMBAR.ALL.CTA).
 __device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
 
-template <int P, bool GENERAL>
+// SYM: the coefficient tensor is symmetric, so K is.  Where a CTA holds all
+// rows of an element (t'-major, NAG == 1) only the blocks with t'-block >=
+// t-block are multiplied; the rest are mirrored from the CTA's staged K.
+template <int P, bool GENERAL, bool SYM>
 __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::MINB)
     sumfact_kernel(LaunchArgs args, SumFactTables tab) {
   using C = SumFactConfig<P>;
+  constexpr bool SYMK = SYM && C::TMAJOR && C::NAG == 1;
   constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ, NTP = C::NTP;
   constexpr int MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
   constexpr int NCHUNK = C::NCHUNK;
@@ -357,7 +361,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
-                  dmma_8x8x4(acc[wa][mt][g * NV + b][0], acc[wa][mt][g * NV + b][1], afr[mt], gv);
+                  if (!SYMK || g >= mt) dmma_8x8x4(acc[wa][mt][g * NV + b][0], acc[wa][mt][g * NV + b][1], afr[mt], gv);
               }
             }
           }
@@ -391,6 +395,49 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     }
 
     // ---- epilogue (overlaps the producers' next item) ----
+    if constexpr (SYMK) {
+      // CTA-wide staging of whole element matrices [EPC][NT*NV][NSH]; blocks
+      // below the t-block diagonal are read back transposed.
+      double* st = smem + C::OFF_STAGE + el_w * (NT * NV * NSH);
+#pragma unroll
+      for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t = mt * 8 + (lane >> 2);
+#pragma unroll
+          for (int g = mt; g < MT; ++g)
+#pragma unroll
+            for (int b = 0; b < NV; ++b)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int tp = g * 8 + 2 * (lane & 3) + h;
+                if (t < NT && tp < NT) st[(t * NV + al0 + wa) * NSH + tp * NV + b] = acc[wa][mt][g * NV + b][h];
+              }
+        }
+      named_sync(kBarCons, 32 * C::NCW);
+      if (e < args.n_elem) {
+#pragma unroll
+        for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int row = t * NV + al0 + wa;
+#pragma unroll
+            for (int j0 = 0; j0 < NSH; j0 += 32) {
+              const int j = j0 + lane;
+              if (j < NSH) {
+                const int tp = j / NV;
+                const double v = (tp >> 3) < (t >> 3) ? st[j * NSH + row] : st[row * NSH + j];
+                if (args.out_layout == PI_OUT_CANONICAL)
+                  args.out[e * kk_elem + static_cast<int64_t>(row) * NSH + j] = v;
+                else
+                  args.out[(static_cast<int64_t>(row) * NSH + j) * args.ld_out + e] = v;
+              }
+            }
+          }
+      }
+      named_sync(kBarCons, 32 * C::NCW);  // staging is rewritten by the next item
+      continue;
+    }
     if (e >= args.n_elem) continue;
     if constexpr (C::TMAJOR) {
       // warp-private staging of its WA*NT full K rows, then row-wise coalesced stores

@@ -62,35 +62,41 @@ template <int P>
 struct SumFactHost {
   using C = SumFactConfig<P>;
   static void set_attrs() {
-    cudaFuncSetAttribute(sumfact_kernel<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sumfact_kernel<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM_BYTES));
-    cudaFuncSetAttribute(sumfact_kernel<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sumfact_kernel<P, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::SMEM_BYTES));
+    cudaFuncSetAttribute(sumfact_kernel<P, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(C::SMEM_BYTES));
   }
   // Persistent grid: as many CTAs as fit on the device at once (queried per
   // instantiation), each looping over (element group, a-group) work items.
-  static int resident_ctas(bool general) {
-    static int cached[2] = {0, 0};
-    int& c = cached[general ? 1 : 0];
+  template <bool G, bool Y>
+  static int resident_ctas() {
+    static int c = 0;
     if (c == 0) {
       int dev = 0, sms = 0, per_sm = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (general)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, true>, C::NTHREADS, C::SMEM_BYTES);
-      else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, false>, C::NTHREADS, C::SMEM_BYTES);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, G, Y>, C::NTHREADS, C::SMEM_BYTES);
       c = std::max(1, sms * std::max(1, per_sm));
     }
     return c;
   }
-  static void launch(const LaunchArgs& a, const SumFactTables& t, bool general, cudaStream_t s) {
+  template <bool G, bool Y>
+  static void go(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
     const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NAG;
-    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas(general))));
-    if (general)
-      sumfact_kernel<P, true><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<G, Y>())));
+    sumfact_kernel<P, G, Y><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+  }
+  // general: full 4x4 tensor; symmetric: the tensor (hence K) is symmetric.
+  static void launch(const LaunchArgs& a, const SumFactTables& t, bool general, bool symmetric, cudaStream_t s) {
+    if (!general)
+      go<false, true>(a, t, s);
+    else if (symmetric)
+      go<true, true>(a, t, s);
     else
-      sumfact_kernel<P, false><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+      go<true, false>(a, t, s);
   }
   // Builds the X fragment table, Y table and rule coordinates from the
   // caller's rule and shape table; false if the table is not the tensor
@@ -178,8 +184,8 @@ bool dispatch_p(int p, Args&&... args) {
 
 template <int P>
 struct LaunchOp {
-  static void run(const LaunchArgs& a, const SumFactTables& t, bool general, cudaStream_t s) {
-    SumFactHost<P>::launch(a, t, general, s);
+  static void run(const LaunchArgs& a, const SumFactTables& t, bool general, bool symmetric, cudaStream_t s) {
+    SumFactHost<P>::launch(a, t, general, symmetric, s);
   }
 };
 template <int P>
@@ -354,7 +360,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   a.out_layout = out_layout;
   a.ld_out = ld_out;
   a.bad = ctx->d_bad;
-  bool general = false;
+  bool general = false, symmetric = true;
   switch (coeff_mode) {
     case PI_COEFF_LAPLACE:
       break;
@@ -362,12 +368,15 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
       if (!coeff) return set_error(err, PI_E_CONTRACT, "uniform coefficient tensor is NULL");
       std::memcpy(a.cu, coeff, sizeof(a.cu));
       general = true;
+      for (int k = 0; k < 4; ++k)
+        for (int l = 0; l < 4; ++l) symmetric = symmetric && a.cu[k * 4 + l] == a.cu[l * 4 + k];
       break;
     case PI_COEFF_PER_ELEMENT:
       if (!coeff || coeff_ld < n_elem) return set_error(err, PI_E_CONTRACT, "per-element coefficients: bad buffer/ld");
       a.coeff = coeff;
       a.coeff_ld = coeff_ld;
       general = true;
+      symmetric = false;
       break;
     default:
       return set_error(err, PI_E_CONFIG, "unknown coefficient mode %d", coeff_mode);
@@ -384,7 +393,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
       p1_thread_kernel<false><<<grid, kP1Threads, 0, s>>>(a, t);
   } else {
     SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
-    dispatch_p<LaunchOp>(ctx->p, a, t, general, s);
+    dispatch_p<LaunchOp>(ctx->p, a, t, general, symmetric, s);
   }
   PI_CUDA(cudaGetLastError(), "kernel launch");
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
