@@ -333,17 +333,22 @@ def main():
         }
     dom = max(ps, key=lambda p: per_p_ms[p])
     d = per_p[str(dom)]
+    # DRAM bytes per launch of the dominant kernel: per-element bytes from the
+    # committed ncu capture (profiles/traffic.json, dram__bytes_read+write)
+    # scaled to this launch's element count.
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.load(open(tf)).get(f"p{dom}_{args.coeff}")
+            per_el = json.load(open(tf)).get(f"p{dom}_{args.coeff}")
+            traffic = per_el * E if per_el is not None else None
         except Exception:
             traffic = None
     roofline = {
         "bound": "tensor", "kernel": f"sumfact_kernel<{dom}> (FP64 DMMA)" if dom >= 2 else "p1_thread_kernel",
         "achieved": d["dense_tflops"], "peak": dmma_tf, "unit": "TFLOP/s", "frac": d["dense_tflops"] / dmma_tf,
-        "traffic": traffic,
+        "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/traffic.json)",
+        "algorithmic_bytes": d["bytes_per_element"] * E,
         "achieved_note": "SURVEY 8(d) dense FLOP_alg per element x elements / kernel time; the kernel "
                          "executes the sum-factorised algorithm with fewer FLOPs, so frac can exceed 1",
         "executed_tflops": d["executed_tflops"], "executed_frac": d["executed_tflops"] / dmma_tf,

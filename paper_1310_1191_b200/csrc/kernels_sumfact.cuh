@@ -48,7 +48,11 @@ struct SumFactShape {
   static constexpr int KSTEPS = 3 * NSP / 4;          // k4-steps over (s, x)
   static constexpr int NCHUNK = NSP / 4;              // 4 triangle points per chunk
   static constexpr int XFRAG = MT * KSTEPS * 32;      // doubles in the A-fragment table
-  static constexpr int XPLAIN = NSP * NTP * 4;        // X as [s][t'][y(4)]
+  // X as [s][y][t'] with a row pitch NTPS = NTP rounded up to 8 (mod 16):
+  // rows s and s+1 then start 64 bytes apart modulo 128, so the two s a
+  // warp reads per k-step land in disjoint bank halves.
+  static constexpr int NTPS = (NTP + 7) / 16 * 16 + 8;
+  static constexpr int XPLAIN = NSP * 3 * NTPS;
 };
 
 // Launch shape: EPC elements x AG Legendre rows `a` per CTA; each consumer
@@ -106,7 +110,9 @@ struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<
   // H for one chunk: [EPC][AG][4 s][NV b][3 x][4 y (padded)]
   static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NV * 12;
   static constexpr int NBUF = 3;  // H ring depth (producers run up to NBUF chunks ahead)
-  static constexpr int M_PER_CHUNK = L::EPC * 4 * S::NZ * 16;
+  static constexpr int MITEMS = L::EPC * 4 * S::NZ;   // points per chunk
+  static constexpr int MPITCH = MITEMS | 1;             // M stored k-major: [16][MPITCH]
+  static constexpr int M_PER_CHUNK = 16 * MPITCH;
   // shared memory layout (doubles; every block 16-byte aligned)
   static constexpr int OFF_XA = 0;
   static constexpr int OFF_XP = OFF_XA + S::XFRAG;
@@ -128,8 +134,8 @@ struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<
 // table, pi_context.cu).
 struct SumFactTables {
   const double* xfrag;   // X in A-fragment order [MT][KSTEPS][32]
-  const double* xplain;  // X as [NSP][NTP][4] (y = 0..2, zero padded)
-  const double* yline;   // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
+  const double* xplain;  // X as [NSP][3][NTPS] (zero padded)
+  const double* yline;   // P [NZ][NV], P' [NZ][NV], xi3 [NZ]
   const double* tri;     // xi1 [NS], xi2 [NS]
   const double* w;       // [NQ] rule weights (reference order)
 };
@@ -152,7 +158,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     sumfact_kernel(LaunchArgs args, SumFactTables tab) {
   using C = SumFactConfig<P>;
   constexpr bool SYMK = SYM && C::TMAJOR && C::NAG == 1;
-  constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ, NTP = C::NTP;
+  constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ, NTPS = C::NTPS;
   constexpr int MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
   constexpr int NCHUNK = C::NCHUNK;
   extern __shared__ __align__(16) double smem[];
@@ -176,8 +182,8 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   for (int i = tid; i < NQ; i += C::NTHREADS) sW[i] = tab.w[i];
   __syncthreads();
 
-  const double* Pv = sY;            // P_a(z)  [NV][NZ]
-  const double* Pd = sY + NV * NZ;  // P'_a(z) [NV][NZ]
+  const double* Pv = sY;            // P_a(z)  [NZ][NV]
+  const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]
 
   // Work items: (element group, a-group); this CTA takes items blockIdx.x + k*gridDim.x.
   const int64_t n_items = (args.n_elem + EPC - 1) / EPC * C::NAG;
@@ -223,9 +229,8 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
             for (int k = 0; k < 16; ++k) M[k] = 0.0;
           }
-          double2* dst = reinterpret_cast<double2*>(sM + i * 16);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) dst[k] = make_double2(M[2 * k], M[2 * k + 1]);
+          for (int k = 0; k < 16; ++k) sM[k * C::MPITCH + i] = M[k];
         }
         named_sync(kBarProd, C::NPT);
         const int buf = static_cast<int>(gc % C::NBUF);
@@ -240,24 +245,25 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           double h[C::BPER][3];
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
-          const double* Mp = sM + (el * 4 + sl) * NZ * 16;
+          const double* Mp = sM + (el * 4 + sl) * NZ;  // M_k of point z at Mp[k*MPITCH + z]
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
-            const double* M = Mp + z * 16;
-            const double pa = Pv[a * NZ + z], da = Pd[a * NZ + z];
+            const double* Mz = Mp + z;
+            auto M = [Mz](int k) { return Mz[k * C::MPITCH]; };
+            const double pa = Pv[z * NV + a], da = Pd[z * NV + a];
             // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
             // plus row 0 weighted by P for x = 2 in the general case)
             const double wr = x < 2 ? pa : da;
             const double w0 = (GENERAL && x == 2) ? pa : 0.0;
-            const double L0 = GENERAL ? wr * M[kx * 4 + 0] + w0 * M[0] : 0.0;
-            const double L1 = wr * M[kx * 4 + 1] + (GENERAL ? w0 * M[1] : 0.0);
-            const double L2 = wr * M[kx * 4 + 2] + (GENERAL ? w0 * M[2] : 0.0);
-            const double L3 = wr * M[kx * 4 + 3] + (GENERAL ? w0 * M[3] : 0.0);
+            const double L0 = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
+            const double L1 = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
+            const double L2 = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
+            const double L3 = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
 #pragma unroll
             for (int bb = 0; bb < C::BPER; ++bb) {
               const int b = bg * C::BPER + bb;
               if (b < NV) {
-                const double pb = Pv[b * NZ + z], db = Pd[b * NZ + z];
+                const double pb = Pv[z * NV + b], db = Pd[z * NV + b];
                 h[bb][0] = fma(L1, pb, h[bb][0]);
                 h[bb][1] = fma(L2, pb, h[bb][1]);
                 h[bb][2] = GENERAL ? fma(L0, pb, fma(L3, db, h[bb][2])) : fma(L3, db, h[bb][2]);
@@ -298,14 +304,29 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     sl_k[ks] = kk / 3;
     x_k[ks] = kk % 3;
   }
-  int hoff[NB], xoff[NB];
+  // Natural order: the warp's n-tiles.  With a symmetric tensor the tiles
+  // entirely below the t-block diagonal are skipped, so tiles are dealt to
+  // warps zig-zag (or strided, when the H register cache needs a fixed b
+  // period) to balance the remaining work.
+  constexpr bool SYMN = SYM && !C::TMAJOR && C::NAG == 1;  // mirrors stay inside the CTA's element
+  int ntl[NB], hoff[NB], xoff[NB];
+  unsigned need[NB];
   if constexpr (!C::TMAJOR) {
+    constexpr bool ZIGZAG = (C::R == 1) || (C::RC == NB);
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      const int j = (nblk * NB + nb) * 8 + cpos;
+      ntl[nb] = SYMN ? (ZIGZAG ? nb * C::NBLK + ((nb & 1) ? C::NBLK - 1 - nblk : nblk) : nb * C::NBLK + nblk)
+                     : nblk * NB + nb;
+      const int j = ntl[nb] * 8 + cpos;
       const int tp = j / NV, b = j - tp * NV;
       hoff[nb] = b * 12;  // + x*4 at use
-      xoff[nb] = tp * 4;  // + s*NTP*4 at use
+      xoff[nb] = tp;      // + s*3*NTPS at use
+      const int tmax = min(NT - 1, (ntl[nb] * 8 + 7) / NV);
+      unsigned m = 0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        if (!SYMN || tmax >= 8 * mt) m |= 1u << mt;
+      need[nb] = m;
     }
   }
 
@@ -343,11 +364,10 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           double xv[MT][3];
 #pragma unroll
           for (int g = 0; g < MT; ++g) {
-            const double* xp = sXP + (s * NTP + g * 8 + cpos) * 4;
-            const double2 x01 = *reinterpret_cast<const double2*>(xp);
-            xv[g][0] = x01.x;
-            xv[g][1] = x01.y;
-            xv[g][2] = xp[2];
+            const double* xp = sXP + s * 3 * NTPS + g * 8 + cpos;
+            xv[g][0] = xp[0];
+            xv[g][1] = xp[NTPS];
+            xv[g][2] = xp[2 * NTPS];
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
@@ -366,7 +386,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
             }
           }
         } else {
-          const double* Xs = sXP + s * NTP * 4;
+          const double* Xs = sXP + s * 3 * NTPS;
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
             const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
@@ -381,12 +401,12 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
             }
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double2 x01 = *reinterpret_cast<const double2*>(Xs + xoff[nb]);
-              const double x2 = Xs[xoff[nb] + 2];
+              const double* xp = Xs + xoff[nb];
               const double* h = hr[nb % C::R];
-              const double gv = fma(h[0], x01.x, fma(h[1], x01.y, h[2] * x2));
+              const double gv = fma(h[0], xp[0], fma(h[1], xp[NTPS], h[2] * xp[2 * NTPS]));
 #pragma unroll
-              for (int mt = 0; mt < MT; ++mt) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], gv);
+              for (int mt = 0; mt < MT; ++mt)
+                if (!SYMN || ((need[nb] >> mt) & 1u)) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], gv);
             }
           }
         }
@@ -482,23 +502,32 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t = mt * 8 + (lane >> 2);
-          if (t >= NT) continue;
           const int row = t * NV + agroup * AG + al0 + wa;
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
-            const int j = (nblk * NB + nb) * 8 + 2 * (lane & 3);
-            if (args.out_layout == PI_OUT_CANONICAL) {
-              double* dst = args.out + e * kk_elem + static_cast<int64_t>(row) * NSH + j;
-              if ((NSH % 2 == 0) && j + 1 < NSH) {
-                *reinterpret_cast<double2*>(dst) = make_double2(acc[wa][mt][nb][0], acc[wa][mt][nb][1]);
-              } else {
-                if (j < NSH) dst[0] = acc[wa][mt][nb][0];
-                if (j + 1 < NSH) dst[1] = acc[wa][mt][nb][1];
+            if (SYMN && !((need[nb] >> mt) & 1u)) continue;  // filled by the transposed tile's mirror
+            if (t >= NT) continue;
+            const int j = ntl[nb] * 8 + 2 * (lane & 3);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int jj = j + h;
+              if (jj >= NSH) continue;
+              const double v = acc[wa][mt][nb][h];
+              bool mirror = false;
+              if (SYMN) {
+                // the transposed entry (jj, row) sits in tile (m-tile of t' = jj/NV, n-tile of row);
+                // write it here when that tile is skipped
+                const int mt2 = (jj / NV) >> 3;
+                const int tmax2 = min(NT - 1, ((row >> 3) * 8 + 7) / NV);
+                mirror = tmax2 < 8 * mt2;
               }
-            } else {
-              const int64_t base = static_cast<int64_t>(row) * NSH + j;
-              if (j < NSH) args.out[base * args.ld_out + e] = acc[wa][mt][nb][0];
-              if (j + 1 < NSH) args.out[(base + 1) * args.ld_out + e] = acc[wa][mt][nb][1];
+              if (args.out_layout == PI_OUT_CANONICAL) {
+                args.out[e * kk_elem + static_cast<int64_t>(row) * NSH + jj] = v;
+                if (mirror) args.out[e * kk_elem + static_cast<int64_t>(jj) * NSH + row] = v;
+              } else {
+                args.out[(static_cast<int64_t>(row) * NSH + jj) * args.ld_out + e] = v;
+                if (mirror) args.out[(static_cast<int64_t>(jj) * NSH + row) * args.ld_out + e] = v;
+              }
             }
           }
         }

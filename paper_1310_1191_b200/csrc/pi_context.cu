@@ -123,8 +123,8 @@ struct SumFactHost {
     yline.assign(2 * NV * NZ + NZ, 0.0);
     for (int a = 0; a < NV; ++a)
       for (int z = 0; z < NZ; ++z) {
-        yline[a * NZ + z] = PHI(z * NS, 0, a);
-        yline[NV * NZ + a * NZ + z] = PHI(z * NS, 3, a);
+        yline[z * NV + a] = PHI(z * NS, 0, a);
+        yline[NV * NZ + z * NV + a] = PHI(z * NS, 3, a);
       }
     for (int z = 0; z < NZ; ++z) yline[2 * NV * NZ + z] = pts[3 * z * NS + 2];
     // X_x(t,s): x=0 dm/dxi1, 1 dm/dxi2, 2 m, read at a=0 (P_0 = 1), z=0.
@@ -142,7 +142,7 @@ struct SumFactHost {
         for (int t = 0; t < NT; ++t)
           for (int a = 0; a < NV; ++a) {
             const int q = z * NS + s, dof = t * NV + a;
-            const double Pz = yline[a * NZ + z], D = yline[NV * NZ + a * NZ + z];
+            const double Pz = yline[z * NV + a], D = yline[NV * NZ + z * NV + a];
             const double m = X[(2 * NT + t) * NS + s];
             const double ref[4] = {m * Pz, X[(0 * NT + t) * NS + s] * Pz, X[(1 * NT + t) * NS + s] * Pz, m * D};
             for (int k = 0; k < 4; ++k) {
@@ -164,7 +164,7 @@ struct SumFactHost {
     xplain.assign(C::XPLAIN, 0.0);
     for (int s = 0; s < NS; ++s)
       for (int t = 0; t < NT; ++t)
-        for (int x = 0; x < 3; ++x) xplain[(static_cast<size_t>(s) * C::NTP + t) * 4 + x] = X[(x * NT + t) * NS + s];
+        for (int x = 0; x < 3; ++x) xplain[(static_cast<size_t>(s) * 3 + x) * C::NTPS + t] = X[(x * NT + t) * NS + s];
     return true;
   }
 };

@@ -1,0 +1,108 @@
+"""Turn a gpurun sweep (ncu launch list CSV) + one full ncu capture into a
+committed summary under profiles/.
+
+  python tools/profile_summary.py <tag> [--full gpurun_out/prof_<tag>_pN.ncu-rep]
+
+Writes profiles/<tag>_launches.csv (copy), profiles/<tag>.md and updates
+profiles/traffic.json (DRAM bytes per launch per (p, coeff), read by bench.py).
+"""
+import argparse
+import csv
+import json
+import shutil
+import subprocess
+import sys
+from collections import OrderedDict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+E_SWEEP = 2 * 128 * 64 * 16  # tools/sweep.sh uses --nz 16
+LAPLACE = {1: 3390, 2: 48402, 3: 531408, 4: 2910080, 5: 14934750, 6: 54773565, 7: 170459184}
+CDR = {1: 4326, 2: 64602, 3: 711888, 4: 3894080, 5: 19962150, 6: 73155621, 7: 227552304}
+NSH = {p: (p + 1) ** 2 * (p + 2) // 2 for p in range(1, 8)}
+FP64_PEAK = 37.0e12  # measured DMMA peak (pi_measure_fp64_peak), TFLOP/s
+HBM_PEAK = 6549.8e9
+
+
+def parse_launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, agg = None, OrderedDict()
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            k = (int(d["ID"]), d["Kernel Name"].split("(")[0])
+            agg.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+    return agg
+
+
+def kernel_key(name):
+    """'void sumfact_kernel<4, 0, 1>' -> (4, 'laplace'); p1_thread_kernel<0> -> (1, 'laplace')."""
+    inside = name.split("<")[1].rstrip(">").replace(" ", "").split(",")
+    if "p1_thread" in name:
+        return 1, "laplace" if inside[0] in ("0", "false") else "cdr"
+    p = int(inside[0])
+    general = inside[1] in ("1", "true")
+    return p, "cdr" if general else "laplace"
+
+
+def full_counters(rep):
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    if len(r) < 3:
+        return {}
+    d = dict(zip(r[0], r[2]))
+    keep = ["Kernel Name", "gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread", "launch__grid_size",
+            "launch__block_size", "dram__bytes_read.sum", "dram__bytes_write.sum"]
+    return {k: d.get(k) for k in keep}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("tag")
+    ap.add_argument("--full", default=None)
+    a = ap.parse_args()
+    src = ROOT / "gpurun_out" / f"sweep_{a.tag}.csv"
+    prof = ROOT / "profiles"
+    prof.mkdir(exist_ok=True)
+    shutil.copy(src, prof / f"{a.tag}_launches.csv")
+    agg = parse_launches(src)
+    seen = {}
+    for (i, name), m in agg.items():
+        key = kernel_key(name)
+        seen.setdefault(key, []).append((name, m))
+    lines = [f"# Kernel sweep `{a.tag}` (1 B200, ncu launch list, {E_SWEEP} prisms per launch, cold/serialised)", "",
+             "Dense roofline = min(FP64 peak 37.0 TF/s / FLOP_alg, HBM 6549.8 GB/s / bytes) per SURVEY.md 8(d).", "",
+             "| p | weak form | kernel | ms | elements/s | vs dense roofline | DRAM read MB | DRAM write MB | K bytes ideal MB |",
+             "|---|---|---|---|---|---|---|---|---|"]
+    traffic = {}
+    tf = prof / "traffic.json"
+    if tf.exists():
+        traffic = json.load(open(tf))
+    for (p, form), lst in sorted(seen.items()):
+        name, m = lst[-1]
+        t = m["gpu__time_duration.sum"] * 1e-9
+        flops = (LAPLACE if form == "laplace" else CDR)[p]
+        byts = 8 * NSH[p] ** 2 + 144 + (128 if form == "cdr" else 0)
+        bound = min(FP64_PEAK / flops, HBM_PEAK / byts)
+        rd, wr = m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
+        lines.append(f"| {p} | {form} | `{name.replace('void ', '')}` | {t*1e3:.3f} | {E_SWEEP/t:.3e} | "
+                     f"{E_SWEEP/t/bound:.2f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {8*NSH[p]**2*E_SWEEP/1e6:.1f} |")
+        traffic[f"p{p}_{form}"] = (rd + wr) / E_SWEEP  # DRAM bytes per element (per launch / elements)
+    json.dump(traffic, open(tf, "w"), indent=1)
+    if a.full:
+        c = full_counters(a.full)
+        lines += ["", f"## Full capture `{Path(a.full).name}`", "", "| counter | value |", "|---|---|"]
+        lines += [f"| {k} | {v} |" for k, v in c.items()]
+    (prof / f"{a.tag}.md").write_text("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
