@@ -100,6 +100,91 @@ __device__ __forceinline__ void coefficient_block(const double inv[3][3], double
   }
 }
 
+
+// Per-element geometry as the seven edge vectors the multilinear map needs
+// (geometry.cpp:32-58): d = [x1-x0, x4-x3, x2-x0, x5-x3, x3-x0, x4-x1, x5-x2],
+// each [3].  Then J[:,0] = zm d0 + zp d1, J[:,1] = zm d2 + zp d3,
+// J[:,2] = (l0 d4 + l1 d5 + l2 d6)/2.
+__device__ __forceinline__ void prism_edges(const double* __restrict__ x, double d[21]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    d[0 + i] = x[3 + i] - x[0 + i];
+    d[3 + i] = x[12 + i] - x[9 + i];
+    d[6 + i] = x[6 + i] - x[0 + i];
+    d[9 + i] = x[15 + i] - x[9 + i];
+    d[12 + i] = x[9 + i] - x[0 + i];
+    d[15 + i] = x[12 + i] - x[3 + i];
+    d[18 + i] = x[15 + i] - x[6 + i];
+  }
+}
+
+// The per-point block M = T (det w C) T^T of coefficient_block, built from
+// the cofactors c_ik of J without forming J^-1 (inv[k][i] = c_ik / det,
+// geometry.cpp:60-83):
+//   Laplace  M_kl = (w/det) sum_i c_i,k-1 c_i,l-1            (k, l >= 1)
+//   general  M_00 = w det C_00,  M_0l = w sum_b C_0b c_b-1,l-1,
+//            M_k0 = w sum_a c_a-1,k-1 C_a0,
+//            M_kl = (w/det) sum_ab c_a-1,k-1 C_ab c_b-1,l-1.
+// Returns det (<= 0 flags an inverted element, geometry.cpp:67-69).
+template <bool GENERAL>
+__device__ __forceinline__ double point_block(const double* __restrict__ d, double xi1, double xi2, double xi3,
+                                              double w, const double* c, double M[16]) {
+  const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
+  const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
+  double j[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    j[i][0] = fma(zm, d[0 + i], zp * d[3 + i]);
+    j[i][1] = fma(zm, d[6 + i], zp * d[9 + i]);
+    j[i][2] = fma(l0, d[12 + i], fma(l1, d[15 + i], l2 * d[18 + i]));
+  }
+  double cf[3][3];  // cf[i][k] = cofactor of J[i][k]
+  cf[0][0] = j[1][1] * j[2][2] - j[1][2] * j[2][1];
+  cf[0][1] = j[1][2] * j[2][0] - j[1][0] * j[2][2];
+  cf[0][2] = j[1][0] * j[2][1] - j[1][1] * j[2][0];
+  cf[1][0] = j[0][2] * j[2][1] - j[0][1] * j[2][2];
+  cf[1][1] = j[0][0] * j[2][2] - j[0][2] * j[2][0];
+  cf[1][2] = j[0][1] * j[2][0] - j[0][0] * j[2][1];
+  cf[2][0] = j[0][1] * j[1][2] - j[0][2] * j[1][1];
+  cf[2][1] = j[0][2] * j[1][0] - j[0][0] * j[1][2];
+  cf[2][2] = j[0][0] * j[1][1] - j[0][1] * j[1][0];
+  const double det = j[0][0] * cf[0][0] + j[0][1] * cf[0][1] + j[0][2] * cf[0][2];
+  const double wd = w * __drcp_rn(det);
+  if (!GENERAL) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int l = k; l < 3; ++l) {
+        const double v = wd * fma(cf[0][k], cf[0][l], fma(cf[1][k], cf[1][l], cf[2][k] * cf[2][l]));
+        M[(k + 1) * 4 + (l + 1)] = v;
+        M[(l + 1) * 4 + (k + 1)] = v;
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      M[k] = 0.0;
+      M[k * 4] = 0.0;
+    }
+  } else {
+    double W[4][3];  // W[a][l-1] = sum_b C_ab c_b-1,l-1
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+        W[a][l] = fma(c[a * 4 + 1], cf[0][l], fma(c[a * 4 + 2], cf[1][l], c[a * 4 + 3] * cf[2][l]));
+    M[0] = w * det * c[0];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) M[l + 1] = w * W[0][l];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      M[(k + 1) * 4] = w * fma(cf[0][k], c[4], fma(cf[1][k], c[8], cf[2][k] * c[12]));
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+        M[(k + 1) * 4 + (l + 1)] = wd * fma(cf[0][k], W[1][l], fma(cf[1][k], W[2][l], cf[2][k] * W[3][l]));
+    }
+  }
+  return det;
+}
+
 __device__ __forceinline__ void flag_inverted(unsigned long long* bad, int64_t gid) {
   atomicMin(bad, static_cast<unsigned long long>(gid));
 }

@@ -38,9 +38,13 @@ __global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, 
   const int64_t e = static_cast<int64_t>(blockIdx.x) * kP1Threads + tid;
   const bool live = e < args.n_elem;
   const int64_t ec = live ? e : args.n_elem - 1;
-  double x[18];
+  double d[21];
+  {
+    double x[18];
 #pragma unroll
-  for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+    for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+    prism_edges(x, d);
+  }
   double cf[16];
   if (GENERAL) {
 #pragma unroll
@@ -54,11 +58,9 @@ __global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, 
 
 #pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
-    double inv[3][3];
-    const double det = prism_jacobian(x, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], inv);
-    inverted |= !(det > 0.0);
     double M[16];
-    coefficient_block<GENERAL>(inv, det * sW[q], cf, M);
+    const double det = point_block<GENERAL>(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], sW[q], cf, M);
+    inverted |= !(det > 0.0);
     const double* ph = sPhi + q * 4 * NSH;
     constexpr int K0 = GENERAL ? 0 : 1;  // Laplace has no value row
     // G_l(i) = sum_k phi_k(i) M_kl ; K_ij += sum_l G_l(i) phi_l(j)

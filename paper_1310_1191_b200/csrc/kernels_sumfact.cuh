@@ -66,7 +66,7 @@ template <> struct SumFactLaunch<2> {
 };
 template <> struct SumFactLaunch<3> {
   static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 4, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 4, BSPLIT = 1, MINB = 1;
+  static constexpr int EPC = 2, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 1, MINB = 2;
 };
 template <> struct SumFactLaunch<4> {
   static constexpr bool TMAJOR = true;
@@ -119,7 +119,7 @@ struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<
   static constexpr int OFF_H = OFF_XP + S::XPLAIN;
   static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
   static constexpr int OFF_GEOM = OFF_M + M_PER_CHUNK;
-  static constexpr int OFF_C = OFF_GEOM + L::EPC * 18;
+  static constexpr int OFF_C = OFF_GEOM + (L::EPC * 21 + 1) / 2 * 2;
   static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
   static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
@@ -198,11 +198,15 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
       const int64_t w = blockIdx.x + it * gridDim.x;
       const int64_t e0 = (w / C::NAG) * EPC;
       const int agroup = static_cast<int>(w % C::NAG);
-      for (int i = ptid; i < EPC * 18; i += C::NPT) {
-        const int el = i / 18, c = i % 18;
-        const int64_t e = e0 + el;
+      if (ptid < EPC) {  // edge vectors of the item's elements
+        const int64_t e = e0 + ptid;
         const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;  // pad with a valid element
-        sGeom[i] = args.geom[c * args.geom_ld + ec];
+        double x[18], d[21];
+#pragma unroll
+        for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+        prism_edges(x, d);
+#pragma unroll
+        for (int c = 0; c < 21; ++c) sGeom[ptid * 21 + c] = d[c];
       }
       if (GENERAL) {
         for (int i = ptid; i < EPC * 16; i += C::NPT) {
@@ -220,11 +224,10 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           const int s = chunk * 4 + sl;
           double M[16];
           if (s < NS) {
-            double inv[3][3];
-            const double det = prism_jacobian(sGeom + 18 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], inv);
+            const double det = point_block<GENERAL>(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z],
+                                                    sW[z * NS + s], sC + 16 * el, M);
             const int64_t e = e0 + el;
             if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
-            coefficient_block<GENERAL>(inv, det * sW[z * NS + s], sC + 16 * el, M);
           } else {
 #pragma unroll
             for (int k = 0; k < 16; ++k) M[k] = 0.0;
@@ -387,6 +390,17 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           }
         } else {
           const double* Xs = sXP + s * 3 * NTPS;
+          // X values of the lane's n-tiles, shared by the WA rows a
+          double xr[WA > 1 ? NB : 1][3];
+          if constexpr (WA > 1) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+              const double* xp = Xs + xoff[nb];
+              xr[nb][0] = xp[0];
+              xr[nb][1] = xp[NTPS];
+              xr[nb][2] = xp[2 * NTPS];
+            }
+          }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
             const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
@@ -401,9 +415,14 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
             }
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double* xp = Xs + xoff[nb];
               const double* h = hr[nb % C::R];
-              const double gv = fma(h[0], xp[0], fma(h[1], xp[NTPS], h[2] * xp[2 * NTPS]));
+              double gv;
+              if constexpr (WA > 1) {
+                gv = fma(h[0], xr[nb][0], fma(h[1], xr[nb][1], h[2] * xr[nb][2]));
+              } else {
+                const double* xp = Xs + xoff[nb];
+                gv = fma(h[0], xp[0], fma(h[1], xp[NTPS], h[2] * xp[2 * NTPS]));
+              }
 #pragma unroll
               for (int mt = 0; mt < MT; ++mt)
                 if (!SYMN || ((need[nb] >> mt) & 1u)) dmma_8x8x4(acc[wa][mt][nb][0], acc[wa][mt][nb][1], afr[mt], gv);
@@ -436,24 +455,28 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
         }
       named_sync(kBarCons, 32 * C::NCW);
       if (e < args.n_elem) {
+        // column chunks of 32: per lane the column j, its t'-block and the
+        // transposed row offset are fixed; rows (t, a) are compile-time.
+        double* orow = args.out + e * kk_elem;
 #pragma unroll
-        for (int wa = 0; wa < WA; ++wa)
+        for (int j0 = 0; j0 < NSH; j0 += 32) {
+          const int j = j0 + lane;
+          if (j < NSH) {
+            const int tblk = (j / NV) >> 3;
+            const double* tr = st + j * NSH;  // transposed source row
 #pragma unroll
-          for (int t = 0; t < NT; ++t) {
-            const int row = t * NV + al0 + wa;
+            for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
-            for (int j0 = 0; j0 < NSH; j0 += 32) {
-              const int j = j0 + lane;
-              if (j < NSH) {
-                const int tp = j / NV;
-                const double v = (tp >> 3) < (t >> 3) ? st[j * NSH + row] : st[row * NSH + j];
+              for (int t = 0; t < NT; ++t) {
+                const int row = t * NV + al0 + wa;
+                const double v = tblk < (t >> 3) ? tr[row] : st[row * NSH + j];
                 if (args.out_layout == PI_OUT_CANONICAL)
-                  args.out[e * kk_elem + static_cast<int64_t>(row) * NSH + j] = v;
+                  orow[row * NSH + j] = v;
                 else
                   args.out[(static_cast<int64_t>(row) * NSH + j) * args.ld_out + e] = v;
               }
-            }
           }
+        }
       }
       named_sync(kBarCons, 32 * C::NCW);  // staging is rewritten by the next item
       continue;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels_dense.cuh"
+#include "kernels_p2.cuh"
 #include "kernels_sumfact.cuh"
 #include "pi_internal.hpp"
 
@@ -27,6 +28,9 @@ struct pi_context {
   double *d_phi = nullptr, *d_pts = nullptr, *d_w = nullptr;
   double *d_xfrag = nullptr, *d_xplain = nullptr, *d_yline = nullptr, *d_tri = nullptr;
   bool tensor_ok = false;
+  bool p2_ok = false;       // p = 2 register-dense kernel available
+  int p2_ctas = 0;
+  double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
   // host streaming path
@@ -293,6 +297,23 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
+  if (p == 2) {
+    std::vector<double> p4(4 * nq);
+    for (int q = 0; q < nq; ++q) {
+      p4[4 * q] = ctx->h_pts[3 * q];
+      p4[4 * q + 1] = ctx->h_pts[3 * q + 1];
+      p4[4 * q + 2] = ctx->h_pts[3 * q + 2];
+      p4[4 * q + 3] = ctx->h_w[q];
+    }
+    if ((st = upload(&ctx->d_pts4, p4, err)) != PI_OK) return fail(st);
+    cudaFuncSetAttribute(p2_lane_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(P2Smem));
+    cudaFuncSetAttribute(p2_lane_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(P2Smem));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2_lane_kernel<false>, 32 * kP2Warps, sizeof(P2Smem));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->p2_ctas = std::max(1, per_sm) * sms;
+    ctx->p2_ok = true;
+  }
   ce = cudaGetLastError();
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "context setup"));
   *out = ctx;
@@ -313,6 +334,7 @@ pi_status pi_context_destroy(pi_context* ctx) {
   cudaFree(ctx->d_yline);
   cudaFree(ctx->d_tri);
   cudaFree(ctx->d_bad);
+  cudaFree(ctx->d_pts4);
   if (ctx->hbuf) cudaFree(ctx->hbuf);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -384,7 +406,26 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int v = resolve_variant(ctx);
-  if (v == PI_VARIANT_DENSE) {
+  // p = 2 with a symmetric derivative-only tensor: the register-dense lane kernel.
+  bool p2_dense = false;
+  if (ctx->p == 2 && v == PI_VARIANT_SUMFACT && ctx->p2_ok && (!general || (symmetric && coeff_mode == PI_COEFF_UNIFORM))) {
+    p2_dense = true;
+    if (general)
+      for (int k = 0; k < 4; ++k) p2_dense = p2_dense && a.cu[k] == 0.0 && a.cu[k * 4] == 0.0;
+  }
+  if (p2_dense) {
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2, ctx->d_phi, sizeof(double) * kP2NQ * 4 * kP2NSH, 0,
+                                    cudaMemcpyDeviceToDevice, s),
+            "upload p=2 shape table");
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_p2, ctx->d_pts4, sizeof(double) * kP2NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
+            "upload p=2 rule");
+    const int64_t groups = (n_elem + 31) / 32;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas));
+    if (general)
+      p2_lane_kernel<true><<<grid, 32 * kP2Warps, sizeof(P2Smem), s>>>(a);
+    else
+      p2_lane_kernel<false><<<grid, 32 * kP2Warps, sizeof(P2Smem), s>>>(a);
+  } else if (v == PI_VARIANT_DENSE) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     const unsigned grid = static_cast<unsigned>((n_elem + kP1Threads - 1) / kP1Threads);
     if (general)

@@ -98,10 +98,10 @@ def test_uniform_tensor_and_layouts(p):
     assert np.array_equal(lap, again), "not bitwise deterministic"
 
 
-@pytest.mark.parametrize("p", [1, 3, 5])
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
 def test_ragged_counts_and_twins(p):
     base = pb.generate_box_mesh(2, 2, 2, 0.2, seed=5)
-    for n in (1, 2, 3, 5, 9):
+    for n in (1, 2, 3, 5, 9, 33, 47):
         mesh = np.concatenate([base] * 2)[:n]
         got = run_gpu(p, mesh, pb.LAPLACE)
         assert np.isfinite(got).all()

@@ -1,10 +1,12 @@
 #!/bin/bash
-# Kernel-time sweep over p (ncu launch list, cold, serialised) + one full profile.
-# usage: tools/sweep.sh <tag> [full_p]
-tag=$1; fp=${2:-4}
+# Kernel-time sweep over p (ncu launch list, cold, serialised) + full profiles.
+# usage: tools/sweep.sh <tag> [full_p ...]
+tag=$1; shift
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/sweep_$tag.csv bash -c "for p in 1 2 3 4 5 6 7; do python tools/prof_run.py --p \$p --nz 16 --launches 2; python tools/prof_run.py --p \$p --nz 16 --launches 2 --coeff cdr; done" > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:sumfact_kernel -s 2 -c 1 -o gpurun_out/prof_${tag}_p$fp \
-  python tools/prof_run.py --p $fp --nz 16 --launches 3 > /dev/null 2>&1
+for fp in "$@"; do
+  ncu --set full --clock-control none --import-source on -k regex:"sumfact_kernel|p1_thread" -s 2 -c 1 -o gpurun_out/prof_${tag}_p$fp \
+    python tools/prof_run.py --p $fp --nz 16 --launches 3 > /dev/null 2>&1
+done
 echo sweep done
