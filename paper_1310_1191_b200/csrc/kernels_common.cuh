@@ -185,6 +185,30 @@ __device__ __forceinline__ double point_block(const double* __restrict__ d, doub
   return det;
 }
 
+
+// ---- TMA bulk store (cp.async.bulk, SASS UBLKCP) from shared to global ----
+__device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Stores n doubles from shared memory to global with the TMA bulk engine:
+// scalar head/tail where the global address is only 8-byte aligned.  The
+// caller guarantees src and dst have the same address modulo 16.
+__device__ __forceinline__ void bulk_store_doubles(double* gdst, const double* ssrc, int n) {
+  int head = (reinterpret_cast<uintptr_t>(gdst) & 15) ? 1 : 0;
+  if (head) gdst[0] = ssrc[0];
+  const int body = (n - head) & ~1;
+  if (body > 0) bulk_store(gdst + head, ssrc + head, static_cast<unsigned>(body) * 8u);
+  if (head + body < n) gdst[n - 1] = ssrc[n - 1];
+}
+
 __device__ __forceinline__ void flag_inverted(unsigned long long* bad, int64_t gid) {
   atomicMin(bad, static_cast<unsigned long long>(gid));
 }

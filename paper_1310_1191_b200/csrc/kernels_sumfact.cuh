@@ -124,9 +124,15 @@ struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
   static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
   // t'-major epilogue: each consumer warp stages its WA*NT K rows
+  // t'-major with whole elements in the CTA: element matrices staged in
+  // canonical order (one spare double to match the global address mod 16)
+  // and stored by the TMA bulk engine.
+  static constexpr bool BULK = L::TMAJOR && NAG == 1;
+  static constexpr int ESTRIDE = (S::NSH * S::NSH + 3) / 2 * 2;
   static constexpr int STAGE_PER_WARP = L::TMAJOR ? (L::WA * S::NT * S::NSH + 1) / 2 * 2 : 0;
   static constexpr int OFF_STAGE = (OFF_W + S::NQ + 1) / 2 * 2;
-  static constexpr int SMEM_DOUBLES = OFF_STAGE + NCW * STAGE_PER_WARP;
+  static constexpr int STAGE_DOUBLES = BULK ? L::EPC * ESTRIDE : NCW * STAGE_PER_WARP;
+  static constexpr int SMEM_DOUBLES = OFF_STAGE + STAGE_DOUBLES;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
 };
 
@@ -334,7 +340,11 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   }
 
   int64_t gc = 0;
-  for (int64_t it = 0; it < my_items; ++it) {
+  for (int64_t it = 0; it <= my_items; ++it) {
+    if (it == my_items) {  // drain the TMA bulk stores before the CTA exits
+      if (C::BULK && tid < EPC) bulk_wait_all();
+      break;
+    }
     const int64_t w = blockIdx.x + it * gridDim.x;
     const int64_t e = (w / C::NAG) * EPC + el_w;
     const int agroup = static_cast<int>(w % C::NAG);
@@ -434,51 +444,58 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     }
 
     // ---- epilogue (overlaps the producers' next item) ----
-    if constexpr (SYMK) {
-      // CTA-wide staging of whole element matrices [EPC][NT*NV][NSH]; blocks
-      // below the t-block diagonal are read back transposed.
-      double* st = smem + C::OFF_STAGE + el_w * (NT * NV * NSH);
+    if constexpr (C::BULK) {
+      // Whole element matrices in canonical order, mirrors included, then one
+      // TMA bulk store per element.
+      const bool bulk = args.out_layout == PI_OUT_CANONICAL && (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
+      if (tid < EPC) bulk_wait_read();  // the issuing threads: previous stores no longer read the staging buffer
+      named_sync(kBarCons, 32 * C::NCW);
+      const int64_t ecl = e < args.n_elem ? e : 0;
+      double* st = smem + C::OFF_STAGE + el_w * C::ESTRIDE + (bulk ? static_cast<int>((ecl * kk_elem) & 1) : 0);
 #pragma unroll
       for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t = mt * 8 + (lane >> 2);
+          const int row = t * NV + al0 + wa;
 #pragma unroll
-          for (int g = mt; g < MT; ++g)
+          for (int g = SYMK ? mt : 0; g < MT; ++g)
 #pragma unroll
             for (int b = 0; b < NV; ++b)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int tp = g * 8 + 2 * (lane & 3) + h;
-                if (t < NT && tp < NT) st[(t * NV + al0 + wa) * NSH + tp * NV + b] = acc[wa][mt][g * NV + b][h];
+                if (t < NT && tp < NT) {
+                  const double v = acc[wa][mt][g * NV + b][h];
+                  st[row * NSH + tp * NV + b] = v;
+                  if (SYMK && g > mt) st[(tp * NV + b) * NSH + row] = v;  // mirror of the skipped block
+                }
               }
         }
+      fence_proxy_async_smem();
       named_sync(kBarCons, 32 * C::NCW);
-      if (e < args.n_elem) {
-        // column chunks of 32: per lane the column j, its t'-block and the
-        // transposed row offset are fixed; rows (t, a) are compile-time.
-        double* orow = args.out + e * kk_elem;
-#pragma unroll
-        for (int j0 = 0; j0 < NSH; j0 += 32) {
-          const int j = j0 + lane;
-          if (j < NSH) {
-            const int tblk = (j / NV) >> 3;
-            const double* tr = st + j * NSH;  // transposed source row
-#pragma unroll
-            for (int wa = 0; wa < WA; ++wa)
-#pragma unroll
-              for (int t = 0; t < NT; ++t) {
-                const int row = t * NV + al0 + wa;
-                const double v = tblk < (t >> 3) ? tr[row] : st[row * NSH + j];
-                if (args.out_layout == PI_OUT_CANONICAL)
-                  orow[row * NSH + j] = v;
-                else
-                  args.out[(static_cast<int64_t>(row) * NSH + j) * args.ld_out + e] = v;
-              }
+      if (bulk) {
+        if (tid < EPC) {
+          const int64_t ee = (w / C::NAG) * EPC + tid;
+          if (ee < args.n_elem) {
+            const double* src = smem + C::OFF_STAGE + tid * C::ESTRIDE + static_cast<int>((ee * kk_elem) & 1);
+            bulk_store_doubles(args.out + ee * kk_elem, src, static_cast<int>(kk_elem));
+            bulk_commit();
+          }
+        }
+      } else {
+        for (int el = 0; el < EPC; ++el) {
+          const int64_t ee = (w / C::NAG) * EPC + el;
+          if (ee >= args.n_elem) break;
+          const double* src = smem + C::OFF_STAGE + el * C::ESTRIDE;
+          for (int i = tid; i < kk_elem; i += 32 * C::NCW) {
+            if (args.out_layout == PI_OUT_CANONICAL)
+              args.out[ee * kk_elem + i] = src[i];
+            else
+              args.out[i * args.ld_out + ee] = src[i];
           }
         }
       }
-      named_sync(kBarCons, 32 * C::NCW);  // staging is rewritten by the next item
       continue;
     }
     if (e >= args.n_elem) continue;

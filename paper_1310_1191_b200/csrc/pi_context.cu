@@ -217,6 +217,35 @@ int resolve_variant(const pi_context* ctx) {
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
 
+// Fraction of the (t, t') pairs whose MMA tiles the symmetric path computes
+// (kernels_sumfact.cuh: t'-major skips t'-blocks below the t-block; natural
+// order skips n-tiles whose largest t' lies below the m-tile).
+template <int P>
+struct SymFracOp {
+  static void run(double& f) {
+    using C = SumFactConfig<P>;
+    if (C::NAG != 1) {
+      f = 1.0;
+      return;
+    }
+    long done = 0;
+    for (int t = 0; t < C::NT; ++t)
+      for (int tp = 0; tp < C::NT; ++tp) {
+        const int mt = t / 8;
+        bool comp;
+        if (C::TMAJOR) {
+          comp = tp / 8 >= mt;
+        } else {
+          // natural: columns j = tp*NV + b; count per (t, t') through b = 0
+          const int nt = (tp * C::NV) / 8;
+          comp = std::min(C::NT - 1, (nt * 8 + 7) / C::NV) >= 8 * mt;
+        }
+        done += comp;
+      }
+    f = static_cast<double>(done) / (C::NT * C::NT);
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -619,20 +648,27 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   const int p = ctx->p;
   const bool general = coeff_mode != PI_COEFF_LAPLACE;
   const double nq = quad_count(p), nsh = shape_count(p);
-  // Per rule point: Jacobian 57, cofactor inverse 42, det*w 1, M block
-  // 36 (Laplace) / 136 (general).
-  const double per_point = 100.0 + (general ? 136.0 : 36.0);
-  if (resolve_variant(ctx) == PI_VARIANT_DENSE) {
+  // Per rule point: Jacobian from edge vectors 21 FMA, cofactors/det 32,
+  // reciprocal ~6, M block 24 (Laplace) / ~100 (general), in FLOPs.
+  const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
+  const int v = resolve_variant(ctx);
+  if (v == PI_VARIANT_DENSE) {
     // G_l(i) = sum_k phi_k M_kl and K_ij += sum_l G_l phi_l (upper triangle for Laplace).
     const double r = general ? 4.0 : 3.0;
     const double pairs = general ? nsh * nsh : nsh * (nsh + 1) / 2;
     return nq * (per_point + 2.0 * r * r * nsh + 2.0 * r * pairs);
   }
+  if (p == 2 && !general && ctx->p2_ok) {
+    // lane kernel: 3 threads x (6 rows x 9 FMA for G, 63 entries x 3 FMA) per point
+    return nq * (per_point + 3.0 * 2.0 * (6 * 9 + 63 * 3));
+  }
   const double nv = p + 1, nt = (p + 1) * (p + 2) / 2.0, ns = tri_point_count(p), nz = p + 1;
   const double h_terms = general ? 16.0 / 9.0 : 1.0;
   const double h = ns * nv * nv * 9.0 * nz * 3.0 * h_terms;
   const double g = ns * 3.0 * nv * nsh * 3.0 * 2.0;
-  const double k = nt * 3.0 * ns * nsh * nv * 2.0;
+  double frac = 1.0;
+  if (!general) dispatch_p<SymFracOp>(p, frac);
+  const double k = nt * 3.0 * ns * nsh * nv * 2.0 * frac;
   return nq * per_point + h + g + k;
 }
 

@@ -43,6 +43,8 @@ def kernel_key(name):
     inside = name.split("<")[1].rstrip(">").replace(" ", "").split(",")
     if "p1_thread" in name:
         return 1, "laplace" if inside[0] in ("0", "false") else "cdr"
+    if "p2_lane" in name:
+        return 2, "laplace" if inside[0] in ("0", "false") else "uniform-sym"
     p = int(inside[0])
     general = inside[1] in ("1", "true")
     return p, "cdr" if general else "laplace"
