@@ -108,10 +108,14 @@ def library():
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
-        raise ImportError(f"{LIB_PATH} not built: run `python __graft_entry__.py` build() or "
+    path = LIB_PATH
+    alt = os.environ.get("PRISM_B200_LIB")  # developer A/B builds (make ... LIB=...)
+    if alt:
+        path = Path(alt) if Path(alt).is_absolute() else LIB_PATH.parent / alt
+    if not path.exists():
+        raise ImportError(f"{path} not built: run `python __graft_entry__.py` build() or "
                           f"`make -C paper_1310_1191_b200`")
-    L = C.CDLL(str(LIB_PATH))
+    L = C.CDLL(str(path))
     E = C.POINTER(_ErrInfo)
     vp = C.c_void_p
     L.pi_shape_count.argtypes = [C.c_int]

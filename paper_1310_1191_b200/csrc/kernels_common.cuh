@@ -126,17 +126,21 @@ __device__ __forceinline__ void prism_edges(const double* __restrict__ x, double
 //            M_k0 = w sum_a c_a-1,k-1 C_a0,
 //            M_kl = (w/det) sum_ab c_a-1,k-1 C_ab c_b-1,l-1.
 // Returns det (<= 0 flags an inverted element, geometry.cpp:67-69).
-template <bool GENERAL>
-__device__ __forceinline__ double point_block(const double* __restrict__ d, double xi1, double xi2, double xi3,
-                                              double w, const double* c, double M[16]) {
+// DS / CS: element strides of the edge-vector and coefficient arrays (1 for
+// per-thread arrays; 32 for lane-interleaved shared-memory arrays).
+template <bool GENERAL, int DS = 1, int CS = 1>
+__device__ __forceinline__ double point_block(const double* __restrict__ dp, double xi1, double xi2, double xi3,
+                                              double w, const double* cp, double M[16]) {
+  auto d = [dp](int i) { return dp[i * DS]; };
+  auto c = [cp](int i) { return cp[i * CS]; };
   const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
   const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
   double j[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    j[i][0] = fma(zm, d[0 + i], zp * d[3 + i]);
-    j[i][1] = fma(zm, d[6 + i], zp * d[9 + i]);
-    j[i][2] = fma(l0, d[12 + i], fma(l1, d[15 + i], l2 * d[18 + i]));
+    j[i][0] = fma(zm, d(0 + i), zp * d(3 + i));
+    j[i][1] = fma(zm, d(6 + i), zp * d(9 + i));
+    j[i][2] = fma(l0, d(12 + i), fma(l1, d(15 + i), l2 * d(18 + i)));
   }
   double cf[3][3];  // cf[i][k] = cofactor of J[i][k]
   cf[0][0] = j[1][1] * j[2][2] - j[1][2] * j[2][1];
@@ -170,13 +174,13 @@ __device__ __forceinline__ double point_block(const double* __restrict__ d, doub
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int l = 0; l < 3; ++l)
-        W[a][l] = fma(c[a * 4 + 1], cf[0][l], fma(c[a * 4 + 2], cf[1][l], c[a * 4 + 3] * cf[2][l]));
-    M[0] = w * det * c[0];
+        W[a][l] = fma(c(a * 4 + 1), cf[0][l], fma(c(a * 4 + 2), cf[1][l], c(a * 4 + 3) * cf[2][l]));
+    M[0] = w * det * c(0);
 #pragma unroll
     for (int l = 0; l < 3; ++l) M[l + 1] = w * W[0][l];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      M[(k + 1) * 4] = w * fma(cf[0][k], c[4], fma(cf[1][k], c[8], cf[2][k] * c[12]));
+      M[(k + 1) * 4] = w * fma(cf[0][k], c(4), fma(cf[1][k], c(8), cf[2][k] * c(12)));
 #pragma unroll
       for (int l = 0; l < 3; ++l)
         M[(k + 1) * 4 + (l + 1)] = wd * fma(cf[0][k], W[1][l], fma(cf[1][k], W[2][l], cf[2][k] * W[3][l]));

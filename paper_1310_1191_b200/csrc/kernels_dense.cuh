@@ -20,14 +20,42 @@ struct DenseTables {
 };
 
 constexpr int kP1Threads = 128;
+#ifndef PI_P1_MINB_GENERAL
+#define PI_P1_MINB_GENERAL 2
+#endif
 
+// Structural zeros of the reference basis (reference_element.cpp:255-266):
+// dof = t*(P+1) + a with triangle monomial t = xi1^e1 xi2^e2 (enumerated by
+// total degree d, then e1 = 0..d, reference_element.cpp:195-205) and
+// Legendre degree a.  d/dxi1 vanishes iff e1 = 0, d/dxi2 iff e2 = 0 and the
+// xi3 derivative iff a = 0; the table holds exact 0.0 there (dm1, dm2 and
+// dleg are assigned 0.0, :218-225, :258-259), which the context checks.
+template <int P>
+struct BasisPattern {
+  static constexpr int NV = P + 1;
+  // branch-free so the optimiser folds it once the callers' loops unroll
+  static constexpr int tri_d(int t) {
+    return (t >= 1) + (t >= 3) + (t >= 6) + (t >= 10) + (t >= 15) + (t >= 21) + (t >= 28);
+  }
+  static constexpr int tri_e1(int t) { return t - tri_d(t) * (tri_d(t) + 1) / 2; }
+  static constexpr int tri_e2(int t) { return tri_d(t) - tri_e1(t); }
+  static constexpr bool nz(int k, int dof) {
+    return k == 0 ? true : k == 1 ? tri_e1(dof / NV) > 0 : k == 2 ? tri_e2(dof / NV) > 0 : (dof % NV) > 0;
+  }
+};
+
+// Thread per element.  K_ij = sum_q sum_kl phi_k(i) M_kl phi_l(j) with the
+// per-point block M (kernels_common.cuh); the basis' structural zeros are
+// skipped at compile time (13 of the 24 phi entries per point are non-zero),
+// so the contraction costs about half the dense loop nest's FMAs.
 template <bool GENERAL>
-__global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, DenseTables tab) {
+__global__ void __launch_bounds__(kP1Threads, GENERAL ? PI_P1_MINB_GENERAL : 4) p1_thread_kernel(LaunchArgs args, DenseTables tab) {
   constexpr int NQ = 6, NSH = 6, KK = NSH * NSH;
+  using BP = BasisPattern<1>;
   __shared__ double sPhi[NQ * 4 * NSH];
   __shared__ double sPts[NQ * 3];
   __shared__ double sW[NQ];
-  __shared__ __align__(16) double sOut[kP1Threads * KK];  // 36 KB staging
+  __shared__ __align__(16) double sOut[kP1Threads * KK + kP1Threads];  // 36 KB staging
 
   const int tid = threadIdx.x;
   for (int i = tid; i < NQ * 4 * NSH; i += kP1Threads) sPhi[i] = tab.phi[i];
@@ -38,14 +66,22 @@ __global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, 
   const int64_t e = static_cast<int64_t>(blockIdx.x) * kP1Threads + tid;
   const bool live = e < args.n_elem;
   const int64_t ec = live ? e : args.n_elem - 1;
-  double d[21];
+  // Per-thread edge vectors (and coefficient tensor) in shared memory, odd
+  // pitch so a warp's accesses are conflict-free; they alias the output
+  // staging buffer, which is only used after the loop.  This keeps the 36
+  // accumulators and their operands in registers without spilling.
+  constexpr int PITCH = GENERAL ? 37 : 21;
+  static_assert(PITCH * kP1Threads <= kP1Threads * KK + kP1Threads, "staging alias");
+  double* d = sOut + tid * PITCH;
+  double* cf = d + 21;
   {
-    double x[18];
+    double x[18], dd[21];
 #pragma unroll
     for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
-    prism_edges(x, d);
+    prism_edges(x, dd);
+#pragma unroll
+    for (int c = 0; c < 21; ++c) d[c] = dd[c];
   }
-  double cf[16];
   if (GENERAL) {
 #pragma unroll
     for (int c = 0; c < 16; ++c) cf[c] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
@@ -71,14 +107,16 @@ __global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, 
       for (int l = K0; l < 4; ++l) {
         double s = 0.0;
 #pragma unroll
-        for (int k = K0; k < 4; ++k) s += ph[k * NSH + i] * M[k * 4 + l];
+        for (int k = K0; k < 4; ++k)
+          if (BP::nz(k, i)) s = fma(ph[k * NSH + i], M[k * 4 + l], s);
         g[l] = s;
       }
 #pragma unroll
       for (int j = GENERAL ? 0 : i; j < NSH; ++j) {
         double s = K[i * NSH + j];
 #pragma unroll
-        for (int l = K0; l < 4; ++l) s += g[l] * ph[l * NSH + j];
+        for (int l = K0; l < 4; ++l)
+          if (BP::nz(l, j)) s = fma(g[l], ph[l * NSH + j], s);
         K[i * NSH + j] = s;
       }
     }
@@ -102,6 +140,7 @@ __global__ void __launch_bounds__(kP1Threads) p1_thread_kernel(LaunchArgs args, 
   // bank conflicts: 36 doubles = 18 x 16 B), then write the CTA's contiguous
   // block of 128 * 288 B with coalesced 16-byte stores.
   double2* so2 = reinterpret_cast<double2*>(sOut);
+  __syncthreads();  // every thread is done with its edge vectors / coefficients
 #pragma unroll
   for (int i = 0; i < KK / 2; ++i) so2[tid * (KK / 2) + i] = make_double2(K[2 * i], K[2 * i + 1]);
   __syncthreads();

@@ -1,20 +1,28 @@
-// p = 2 symmetric weak forms (Laplace, symmetric uniform tensors): dense
-// per-point accumulation in registers, lane = element.
+// p = 2: dense per-point accumulation with the basis' structural zeros
+// skipped at compile time, lane = element.
 //
 // At p = 2 the sum-factorised MMA path feeds each tensor-core fragment from
 // three shared-memory loads (the triangle factor has only 6 rows, so every
-// G value is used by one MMA) and is shared-memory bound.  Here each group of
-// 32 elements is handled by 3 warps; lane l of every warp owns element l, and
-// warp r owns the upper-triangle part of the row blocks (r, 5-r) of 3 rows
-// each (63 accumulators, balanced).  Per rule point a thread forms
-// G_l(i) = sum_k phi_k(i) M_kl for its 6 rows and K_ij += sum_l G_l(i) phi_l(j);
-// phi is read with warp-uniform addresses from the constant bank, M (per
-// element and point) is built once by the group and shared through shared
-// memory.  The 32 elements' matrices are staged in shared memory (mirroring
-// the lower triangle) and leave as one contiguous coalesced block.
+// G value is used by one MMA) and is shared-memory bound.  The dense loop
+// nest of integrate_generic (integrate_ref.cpp:72-89) in reference
+// coordinates, K_ij += sum_kl phi_k(i) M_kl phi_l(j), is cheaper here once
+// the zeros of the reference basis are skipped (BasisPattern: 2/3 of the
+// d/dxi entries vanish on average), so it runs on the FP64 FMA pipe:
+//
+//  * a CTA integrates groups of 32 elements; lane l of every warp owns
+//    element l of the group;
+//  * symmetric tensors: warp w (of 9) owns the upper-triangle parts of K
+//    rows w and 17-w (19 accumulators, mirrored at the store); general
+//    tensors: warp w (of 18) owns row w (18 accumulators);
+//  * the per-point blocks M (kernels_common.cuh) of the 18 rule points are
+//    computed once per element into shared memory;
+//  * phi is read with warp-uniform addresses from the constant bank;
+//  * element matrices leave through shared-memory staging (reusing the M
+//    buffer) as contiguous, coalesced blocks.
 #pragma once
 
 #include "kernels_common.cuh"
+#include "kernels_dense.cuh"
 
 namespace pib {
 
@@ -22,79 +30,186 @@ constexpr int kP2NQ = 18, kP2NSH = 18, kP2KK = kP2NSH * kP2NSH;
 __constant__ double c_phi_p2[kP2NQ * 4 * kP2NSH];  // tabulate_shapes order [q][k][dof]
 __constant__ double c_pts_p2[kP2NQ * 4];           // xi1, xi2, xi3, w
 
-constexpr int kP2Warps = 3;
-constexpr int kP2Pitch = kP2KK + 1;  // odd pitch: lanes (elements) hit distinct banks
+constexpr int kP2Pitch = kP2KK + 1;  // odd pitch: staged elements hit distinct banks
 
-struct P2Smem {
-  double M[kP2NQ][6][32];           // Laplace-type symmetric block (k,l = 1..3), per point and lane
-  double D[21][32];                 // edge vectors per lane
-  double K[16 * kP2Pitch];          // staged element matrices (half of the lanes at a time)
+// GENERAL: full 4x4 tensor (uniform in args.cu, or per element in
+// args.coeff); SYM: the tensor is symmetric, so K is (upper triangle only).
+//  SYM:  9 warps, warp w owns rows (w, 17-w)  -> 19 accumulators per lane;
+//  !SYM: 18 warps, warp w owns row w          -> 18 accumulators per lane.
+template <bool GENERAL, bool SYM>
+struct P2Cfg {
+  static constexpr int NW = SYM ? 9 : 18;
+  static constexpr int NR = SYM ? 2 : 1;                 // rows per warp
+  static constexpr int NACC = SYM ? kP2NSH + 1 : kP2NSH;
+  static constexpr int NTHREADS = 32 * NW;
+  static constexpr int NM = GENERAL ? 16 : 6;            // stored M entries per point
+  static constexpr int ROUND = SYM ? 8 : 16;             // elements staged per output round
+  static constexpr int MBUF = kP2NQ * NM * 32;           // doubles
+  static constexpr int SBUF = ROUND * kP2Pitch;
+  static constexpr int BUF = MBUF > SBUF ? MBUF : SBUF;
+  static constexpr int OFF_D = BUF;                      // edge vectors [21][32]
+  static constexpr int OFF_C = OFF_D + 21 * 32;          // coefficients [16][32]
+  static constexpr int SMEM_DOUBLES = OFF_C + (GENERAL ? 16 * 32 : 0);
+  static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
+  // per-SMSP register file (16K regs; warps dealt round-robin to the 4 SMSPs):
+  // 9-warp CTAs x3 need <= 72 registers, one 18-warp CTA <= 96
+  static constexpr int MAXREG = SYM ? 72 : 96;
 };
 
-template <int R>
-__device__ __forceinline__ void p2_accumulate(const P2Smem& sm, int lane, double acc[63]) {
-  // row blocks (R, 5-R): rows 3R..3R+2 with columns >= 3R, rows 15-3R.. with columns >= 15-3R
-  constexpr int RA = 3 * R, RB = 15 - 3 * R;
-  constexpr int NA = 3 * (kP2NSH - RA), NB = 3 * (kP2NSH - RB);
-  static_assert(NA + NB == 63, "balanced blocks");
+// M entry (k, l) of the lane's element at point q; Laplace stores the
+// symmetric 3x3 derivative block [11, 12, 13, 22, 23, 33].
+template <bool GENERAL>
+__device__ __forceinline__ int p2_mslot(int k, int l) {
+  if (GENERAL) return k * 4 + l;
+  const int a = (k < l ? k : l) - 1, b = (k < l ? l : k) - 1;
+  return a == 0 ? b : (a == 1 ? 2 + b : 5);
+}
+
+template <int NR, int W>
+__device__ __forceinline__ constexpr int p2_row(int r) {
+  return NR == 1 ? W : (r == 0 ? W : kP2NSH - 1 - W);
+}
+
+// The warp's rows over all rule points.
+template <bool GENERAL, bool SYM, int W>
+__device__ __forceinline__ void p2_rows(const double* __restrict__ sM, int lane, double* acc) {
+  using BP = BasisPattern<2>;
+  using C = P2Cfg<GENERAL, SYM>;
+  constexpr int K0 = GENERAL ? 0 : 1, NR = C::NR, NM = C::NM;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
-    double m[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) m[k] = sm.M[q][k][lane];
     const double* ph = c_phi_p2 + q * 4 * kP2NSH;
-    // M (symmetric 3x3): m = [11, 12, 13, 22, 23, 33]
-    auto Ml = [&](int k, int l) {
-      const int a = k < l ? k : l, b = k < l ? l : k;
-      return a == 0 ? m[b] : (a == 1 ? m[2 + b] : m[5]);
-    };
+    const double* mq = sM + q * NM * 32 + lane;
+    // G_l(i) = sum_k phi_k(i) M_kl, M read one row k at a time (only the
+    // rows k the warp's basis functions do not annihilate)
+    double g[NR][4];
 #pragma unroll
-    for (int blk = 0; blk < 2; ++blk) {
-      const int r0 = blk == 0 ? RA : RB;
-      const int off = blk == 0 ? 0 : NA;
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int ii = 0; ii < 3; ++ii) {
-        const int i = r0 + ii;
-        double g[3];
+      for (int l = 0; l < 4; ++l) g[r][l] = 0.0;
 #pragma unroll
-        for (int l = 0; l < 3; ++l)
-          g[l] = fma(ph[1 * kP2NSH + i], Ml(0, l), fma(ph[2 * kP2NSH + i], Ml(1, l), ph[3 * kP2NSH + i] * Ml(2, l)));
+    for (int k = K0; k < 4; ++k) {
+      bool need = false;
 #pragma unroll
-        for (int j = r0; j < kP2NSH; ++j) {
-          double& a = acc[off + ii * (kP2NSH - r0) + (j - r0)];
-          a = fma(g[0], ph[1 * kP2NSH + j], fma(g[1], ph[2 * kP2NSH + j], fma(g[2], ph[3 * kP2NSH + j], a)));
+      for (int r = 0; r < NR; ++r) need = need || BP::nz(k, p2_row<NR, W>(r));
+      if (!need) continue;
+      double mk[4];
+#pragma unroll
+      for (int l = K0; l < 4; ++l) mk[l] = mq[p2_mslot<GENERAL>(k, l) * 32];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int i = p2_row<NR, W>(r);
+        if (BP::nz(k, i)) {
+          const double f = ph[k * kP2NSH + i];
+#pragma unroll
+          for (int l = K0; l < 4; ++l) g[r][l] = fma(f, mk[l], g[r][l]);
         }
       }
+    }
+    int off = 0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int i = p2_row<NR, W>(r);
+#pragma unroll
+      for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
+        double s = acc[off + j - (SYM ? i : 0)];
+#pragma unroll
+        for (int l = K0; l < 4; ++l)
+          if (BP::nz(l, j)) s = fma(g[r][l], ph[l * kP2NSH + j], s);
+        acc[off + j - (SYM ? i : 0)] = s;
+      }
+      off += SYM ? kP2NSH - i : kP2NSH;
     }
   }
 }
 
-template <int R>
-__device__ __forceinline__ void p2_stage(P2Smem& sm, int slot, const double acc[63]) {
-  constexpr int RA = 3 * R, RB = 15 - 3 * R, NA = 3 * (kP2NSH - RA);
-  double* k = sm.K + slot * kP2Pitch;
+// General (non-symmetric) tensors: every warp owns one full row i (runtime,
+// warp-uniform), so all 18 warps run the same instruction stream: G is
+// formed densely from the warp-uniform phi_k(i), the column loop skips the
+// structural zeros of phi_l(j) at compile time.
+__device__ __forceinline__ void p2_row_general(const double* __restrict__ sM, int lane, int i, double* acc) {
+  using BP = BasisPattern<2>;
+#pragma unroll 1
+  for (int q = 0; q < kP2NQ; ++q) {
+    const double* ph = c_phi_p2 + q * 4 * kP2NSH;
+    const double* mq = sM + q * 16 * 32 + lane;
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-  for (int blk = 0; blk < 2; ++blk) {
-    const int r0 = blk == 0 ? RA : RB;
-    const int off = blk == 0 ? 0 : NA;
+    for (int k = 0; k < 4; ++k) {
+      const double f = ph[k * kP2NSH + i];
+      if (f != 0.0) {  // warp-uniform: skips the M rows the basis function annihilates
 #pragma unroll
-    for (int ii = 0; ii < 3; ++ii)
-#pragma unroll
-      for (int j = r0; j < kP2NSH; ++j) {
-        const int i = r0 + ii;
-        const double v = acc[off + ii * (kP2NSH - r0) + (j - r0)];
-        k[i * kP2NSH + j] = v;
-        if (j >= r0 + 3) k[j * kP2NSH + i] = v;  // mirror outside the diagonal block
+        for (int l = 0; l < 4; ++l) g[l] = fma(f, mq[(k * 4 + l) * 32], g[l]);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < kP2NSH; ++j) {
+      double s = acc[j];
+#pragma unroll
+      for (int l = 0; l < 4; ++l)
+        if (BP::nz(l, j)) s = fma(g[l], ph[l * kP2NSH + j], s);
+      acc[j] = s;
+    }
   }
 }
 
-// SYMMETRIC coefficient tensors only (Laplace, or a symmetric UNIFORM
-// tensor with no value-row terms, checked by the launcher).
-template <bool GENERAL>
-__global__ void __launch_bounds__(32 * kP2Warps) p2_lane_kernel(LaunchArgs args) {
-  extern __shared__ __align__(16) unsigned char p2_smem_raw[];
-  P2Smem& sm = *reinterpret_cast<P2Smem*>(p2_smem_raw);
+// Writes the lane's accumulators as rows of its staged element matrix.
+template <bool SYM, int NR, int W>
+__device__ __forceinline__ void p2_stage(double* st, const double* acc) {
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int i = p2_row<NR, W>(r);
+#pragma unroll
+    for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
+      const double v = acc[off + j - (SYM ? i : 0)];
+      st[i * kP2NSH + j] = v;
+      if (SYM && j > i) st[j * kP2NSH + i] = v;
+    }
+    off += SYM ? kP2NSH - i : kP2NSH;
+  }
+}
+
+template <bool SYM, int NR, int W>
+__device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, const double* acc) {
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int i = p2_row<NR, W>(r);
+#pragma unroll
+    for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
+      const double v = acc[off + j - (SYM ? i : 0)];
+      args.out[(i * kP2NSH + j) * args.ld_out + e] = v;
+      if (SYM && j > i) args.out[(j * kP2NSH + i) * args.ld_out + e] = v;
+    }
+    off += SYM ? kP2NSH - i : kP2NSH;
+  }
+}
+
+// warp -> compile-time row set (only the NW cases of the instantiation are
+// emitted, keeping the kernel within the instruction cache)
+// warp -> compile-time row pair (symmetric tensors)
+#define P2_WARP_SWITCH(CALL) \
+  switch (warp) {            \
+    case 0: CALL(0); break;  \
+    case 1: CALL(1); break;  \
+    case 2: CALL(2); break;  \
+    case 3: CALL(3); break;  \
+    case 4: CALL(4); break;  \
+    case 5: CALL(5); break;  \
+    case 6: CALL(6); break;  \
+    case 7: CALL(7); break;  \
+    default: CALL(8); break; \
+  }
+
+template <bool GENERAL, bool SYM>
+__global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(LaunchArgs args) {
+  using C = P2Cfg<GENERAL, SYM>;
+  constexpr int NR = C::NR;
+  extern __shared__ __align__(16) double p2_smem[];
+  double* sM = p2_smem;  // M [q][NM][32], then the output staging
+  double* sD = p2_smem + C::OFF_D;
+  double* sC = p2_smem + C::OFF_C;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t groups = (args.n_elem + 31) / 32;
   for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
@@ -107,67 +222,83 @@ __global__ void __launch_bounds__(32 * kP2Warps) p2_lane_kernel(LaunchArgs args)
       for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
       prism_edges(x, d);
 #pragma unroll
-      for (int c = 0; c < 21; ++c) sm.D[c][lane] = d[c];
+      for (int c = 0; c < 21; ++c) sD[c * 32 + lane] = d[c];
+    } else if (GENERAL && warp == 1) {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) sC[c * 32 + lane] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
     }
     __syncthreads();
-    // M for the 18 points, 6 per warp
+    // M for the 18 points (18 / NW per warp)
     {
-      double d[21];
-#pragma unroll
-      for (int c = 0; c < 21; ++c) d[c] = sm.D[c][lane];
       bool inverted = false;
-#pragma unroll 1
-      for (int q = warp; q < kP2NQ; q += kP2Warps) {
+#pragma unroll
+      for (int q = warp; q < kP2NQ; q += C::NW) {
         double M[16];
-        const double det = point_block<GENERAL>(d, c_pts_p2[4 * q], c_pts_p2[4 * q + 1], c_pts_p2[4 * q + 2],
-                                                c_pts_p2[4 * q + 3], args.cu, M);
+        const double det = point_block<GENERAL, 32, 32>(sD + lane, c_pts_p2[4 * q], c_pts_p2[4 * q + 1],
+                                                        c_pts_p2[4 * q + 2], c_pts_p2[4 * q + 3], sC + lane, M);
         inverted |= !(det > 0.0);
-        sm.M[q][0][lane] = M[5];
-        sm.M[q][1][lane] = M[6];
-        sm.M[q][2][lane] = M[7];
-        sm.M[q][3][lane] = M[10];
-        sm.M[q][4][lane] = M[11];
-        sm.M[q][5][lane] = M[15];
+        if (GENERAL) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) sM[(q * 16 + k) * 32 + lane] = M[k];
+        } else {
+          const int src[6] = {5, 6, 7, 10, 11, 15};
+#pragma unroll
+          for (int k = 0; k < 6; ++k) sM[(q * 6 + k) * 32 + lane] = M[src[k]];
+        }
       }
       if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
     }
     __syncthreads();
-    double acc[63];
+    double acc[C::NACC];
 #pragma unroll
-    for (int i = 0; i < 63; ++i) acc[i] = 0.0;
-    if (warp == 0)
-      p2_accumulate<0>(sm, lane, acc);
-    else if (warp == 1)
-      p2_accumulate<1>(sm, lane, acc);
-    else
-      p2_accumulate<2>(sm, lane, acc);
-    // two rounds of 16 elements through the staging buffer
+    for (int i = 0; i < C::NACC; ++i) acc[i] = 0.0;
+    if constexpr (SYM) {
+#define P2_ACC(W) p2_rows<GENERAL, SYM, W>(sM, lane, acc)
+      P2_WARP_SWITCH(P2_ACC)
+#undef P2_ACC
+    } else {
+      p2_row_general(sM, lane, warp, acc);
+    }
+    __syncthreads();  // M no longer read: the buffer becomes the output staging
+    if (args.out_layout == PI_OUT_SOA) {
+      if (live) {
+        if constexpr (SYM) {
+#define P2_SOA(W) p2_store_soa<SYM, NR, W>(args, e, acc)
+          P2_WARP_SWITCH(P2_SOA)
+#undef P2_SOA
+        } else {
+#pragma unroll
+          for (int j = 0; j < kP2NSH; ++j) args.out[(warp * kP2NSH + j) * args.ld_out + e] = acc[j];
+        }
+      }
+      continue;
+    }
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      if ((lane >> 4) == h) {
-        if (warp == 0)
-          p2_stage<0>(sm, lane & 15, acc);
-        else if (warp == 1)
-          p2_stage<1>(sm, lane & 15, acc);
-        else
-          p2_stage<2>(sm, lane & 15, acc);
+    for (int h = 0; h < 32 / C::ROUND; ++h) {
+      if (lane / C::ROUND == h) {
+        double* st = sM + (lane % C::ROUND) * kP2Pitch;
+        if constexpr (SYM) {
+#define P2_STAGE(W) p2_stage<SYM, NR, W>(st, acc)
+          P2_WARP_SWITCH(P2_STAGE)
+#undef P2_STAGE
+        } else {
+#pragma unroll
+          for (int j = 0; j < kP2NSH; ++j) st[warp * kP2NSH + j] = acc[j];
+        }
       }
       __syncthreads();
-      const int64_t first = g * 32 + 16 * h;
+      const int64_t first = g * 32 + C::ROUND * h;
       const int64_t left = args.n_elem - first;
-      const int n_here = left <= 0 ? 0 : (left < 16 ? static_cast<int>(left) : 16);
-      for (int el = 0; el < n_here; ++el) {
-        const double* src = sm.K + el * kP2Pitch;
-        if (args.out_layout == PI_OUT_CANONICAL) {
-          double* dst = args.out + (first + el) * kP2KK;
-          for (int r = threadIdx.x; r < kP2KK; r += 32 * kP2Warps) dst[r] = src[r];
-        } else {
-          for (int r = threadIdx.x; r < kP2KK; r += 32 * kP2Warps) args.out[r * args.ld_out + first + el] = src[r];
-        }
+      const int n_here = left <= 0 ? 0 : (left < C::ROUND ? static_cast<int>(left) : C::ROUND);
+      double* dst = args.out + first * kP2KK;
+      for (int r = threadIdx.x; r < n_here * kP2KK; r += C::NTHREADS) {
+        const int el = r / kP2KK, c = r - el * kP2KK;
+        dst[r] = sM[el * kP2Pitch + c];
       }
       __syncthreads();
     }
   }
 }
+#undef P2_WARP_SWITCH
 
 }  // namespace pib

@@ -29,7 +29,7 @@ struct pi_context {
   double *d_xfrag = nullptr, *d_xplain = nullptr, *d_yline = nullptr, *d_tri = nullptr;
   bool tensor_ok = false;
   bool p2_ok = false;       // p = 2 register-dense kernel available
-  int p2_ctas = 0;
+  int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
   double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
@@ -213,7 +213,7 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
 
 int resolve_variant(const pi_context* ctx) {
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
-  if (ctx->p == 1) return PI_VARIANT_DENSE;
+  if (ctx->p <= 2) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
 
@@ -310,6 +310,20 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   ce = cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
 
+  // The kernels skip the basis' structural zeros (BasisPattern): the table
+  // must hold exact zeros there, as tabulate_shapes does.
+  for (int q = 0; q < nq; ++q)
+    for (int k = 1; k < 4; ++k)
+      for (int dof = 0; dof < nsh; ++dof) {
+        const int t = dof / (p + 1), a = dof % (p + 1);
+        int d = 0, r = t;
+        while (r > d) r -= ++d;
+        const bool nz = k == 1 ? r > 0 : k == 2 ? (d - r) > 0 : a > 0;
+        if (!nz && ctx->h_phi[(static_cast<size_t>(q) * 4 + k) * nsh + dof] != 0.0)
+          return fail(set_error(err, PI_E_CONFIG,
+                                "shape table entry (q=%d, d=%d, dof=%d) is not the reference basis' structural zero",
+                                q, k, dof));
+      }
   if (p >= 2) {
     std::vector<double> xf, xp, yl, tr;
     bool ok = false;
@@ -335,12 +349,22 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
       p4[4 * q + 3] = ctx->h_w[q];
     }
     if ((st = upload(&ctx->d_pts4, p4, err)) != PI_OK) return fail(st);
-    cudaFuncSetAttribute(p2_lane_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(P2Smem));
-    cudaFuncSetAttribute(p2_lane_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(P2Smem));
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2_lane_kernel<false>, 32 * kP2Warps, sizeof(P2Smem));
+    cudaFuncSetAttribute(p2_lane_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<false, true>::SMEM_BYTES));
+    cudaFuncSetAttribute(p2_lane_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, true>::SMEM_BYTES));
+    cudaFuncSetAttribute(p2_lane_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, false>::SMEM_BYTES));
+    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    ctx->p2_ctas = std::max(1, per_sm) * sms;
+    auto ctas = [&](auto kern, int threads, size_t smem) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+      return std::max(1, per_sm) * sms;
+    };
+    ctx->p2_ctas[0] = ctas(p2_lane_kernel<false, true>, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES);
+    ctx->p2_ctas[1] = ctas(p2_lane_kernel<true, true>, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES);
+    ctx->p2_ctas[2] = ctas(p2_lane_kernel<true, false>, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES);
     ctx->p2_ok = true;
   }
   ce = cudaGetLastError();
@@ -376,8 +400,8 @@ pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* er
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
-  if (variant == PI_VARIANT_DENSE && ctx->p != 1)
-    return set_error(err, PI_E_CONFIG, "dense variant is built for p = 1 only in this release");
+  if (variant == PI_VARIANT_DENSE && ctx->p > 2)
+    return set_error(err, PI_E_CONFIG, "dense variant is built for p <= 2 only in this release");
   ctx->variant = variant;
   return PI_OK;
 }
@@ -435,25 +459,21 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int v = resolve_variant(ctx);
-  // p = 2 with a symmetric derivative-only tensor: the register-dense lane kernel.
-  bool p2_dense = false;
-  if (ctx->p == 2 && v == PI_VARIANT_SUMFACT && ctx->p2_ok && (!general || (symmetric && coeff_mode == PI_COEFF_UNIFORM))) {
-    p2_dense = true;
-    if (general)
-      for (int k = 0; k < 4; ++k) p2_dense = p2_dense && a.cu[k] == 0.0 && a.cu[k * 4] == 0.0;
-  }
-  if (p2_dense) {
+  if (ctx->p == 2 && v == PI_VARIANT_DENSE) {
     PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2, ctx->d_phi, sizeof(double) * kP2NQ * 4 * kP2NSH, 0,
                                     cudaMemcpyDeviceToDevice, s),
             "upload p=2 shape table");
     PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_p2, ctx->d_pts4, sizeof(double) * kP2NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
             "upload p=2 rule");
     const int64_t groups = (n_elem + 31) / 32;
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas));
-    if (general)
-      p2_lane_kernel<true><<<grid, 32 * kP2Warps, sizeof(P2Smem), s>>>(a);
+    const int which = !general ? 0 : (symmetric ? 1 : 2);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas[which]));
+    if (!general)
+      p2_lane_kernel<false, true><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
+    else if (symmetric)
+      p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
     else
-      p2_lane_kernel<false><<<grid, 32 * kP2Warps, sizeof(P2Smem), s>>>(a);
+      p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
   } else if (v == PI_VARIANT_DENSE) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     const unsigned grid = static_cast<unsigned>((n_elem + kP1Threads - 1) / kP1Threads);
@@ -653,14 +673,24 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
   const int v = resolve_variant(ctx);
   if (v == PI_VARIANT_DENSE) {
-    // G_l(i) = sum_k phi_k M_kl and K_ij += sum_l G_l phi_l (upper triangle for Laplace).
-    const double r = general ? 4.0 : 3.0;
-    const double pairs = general ? nsh * nsh : nsh * (nsh + 1) / 2;
-    return nq * (per_point + 2.0 * r * r * nsh + 2.0 * r * pairs);
-  }
-  if (p == 2 && !general && ctx->p2_ok) {
-    // lane kernel: 3 threads x (6 rows x 9 FMA for G, 63 entries x 3 FMA) per point
-    return nq * (per_point + 3.0 * 2.0 * (6 * 9 + 63 * 3));
+    // G_l(i) = sum_k phi_k(i) M_kl and K_ij += sum_l G_l(i) phi_l(j) over the
+    // basis' structural non-zeros (BasisPattern); upper triangle when K is
+    // symmetric (Laplace; p = 2 also symmetric uniform tensors -- counted as
+    // the per-element case here).
+    const int n = static_cast<int>(nsh), k0 = general ? 0 : 1;
+    auto nz = [&](int k, int dof) {
+      const int t = dof / (p + 1), a = dof % (p + 1);
+      int d = 0, r = t;
+      while (r > d) r -= ++d;
+      return k == 0 ? true : k == 1 ? r > 0 : k == 2 ? (d - r) > 0 : a > 0;
+    };
+    double fma_count = 0.0;
+    for (int i = 0; i < n; ++i) {
+      for (int k = k0; k < 4; ++k) fma_count += nz(k, i) ? (4 - k0) : 0;
+      for (int j = general ? 0 : i; j < n; ++j)
+        for (int l = k0; l < 4; ++l) fma_count += nz(l, j) ? 1 : 0;
+    }
+    return nq * (per_point + 2.0 * fma_count);
   }
   const double nv = p + 1, nt = (p + 1) * (p + 2) / 2.0, ns = tri_point_count(p), nz = p + 1;
   const double h_terms = general ? 16.0 / 9.0 : 1.0;
