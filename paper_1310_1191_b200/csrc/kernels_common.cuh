@@ -190,6 +190,15 @@ __device__ __forceinline__ double point_block(const double* __restrict__ dp, dou
 }
 
 
+// ---- asynchronous global -> shared copies (cp.async, SASS LDGSTS) ----
+__device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ---- TMA bulk store (cp.async.bulk, SASS UBLKCP) from shared to global ----
 __device__ __forceinline__ void bulk_store(double* gdst, const double* ssrc, unsigned bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));

@@ -48,8 +48,9 @@ struct P2Cfg {
   static constexpr int SBUF = ROUND * kP2Pitch;
   static constexpr int BUF = MBUF > SBUF ? MBUF : SBUF;
   static constexpr int OFF_D = BUF;                      // edge vectors [21][32]
-  static constexpr int OFF_C = OFF_D + 21 * 32;          // coefficients [16][32]
-  static constexpr int SMEM_DOUBLES = OFF_C + (GENERAL ? 16 * 32 : 0);
+  static constexpr int OFF_G = OFF_D + 21 * 32;          // raw geometry, double buffered [2][18][32]
+  static constexpr int OFF_C = OFF_G + 2 * 18 * 32;      // coefficients, double buffered [2][16][32]
+  static constexpr int SMEM_DOUBLES = OFF_C + (GENERAL ? 2 * 16 * 32 : 0);
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
   // per-SMSP register file (16K regs; warps dealt round-robin to the 4 SMSPs):
   // 9-warp CTAs x3 need <= 72 registers, one 18-warp CTA <= 96
@@ -209,23 +210,44 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
   extern __shared__ __align__(16) double p2_smem[];
   double* sM = p2_smem;  // M [q][NM][32], then the output staging
   double* sD = p2_smem + C::OFF_D;
-  double* sC = p2_smem + C::OFF_C;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t groups = (args.n_elem + 31) / 32;
-  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+  // The next group's geometry (warp 0) and coefficients (warp 1) stream into
+  // shared memory with cp.async while the current group is integrated; each
+  // lane copies and later reads its own element's values.
+  auto prefetch = [&](int64_t g, int buf) {
+    const int64_t ec = min(g * 32 + lane, args.n_elem - 1);
+    if (warp == 0) {
+      double* dst = p2_smem + C::OFF_G + buf * 18 * 32 + lane;
+#pragma unroll
+      for (int c = 0; c < 18; ++c) cp_async8(dst + c * 32, args.geom + c * args.geom_ld + ec);
+    } else if (GENERAL && warp == 1 && args.coeff) {
+      double* dst = p2_smem + C::OFF_C + buf * 16 * 32 + lane;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) cp_async8(dst + c * 32, args.coeff + c * args.coeff_ld + ec);
+    }
+    cp_async_commit();
+  };
+  if (blockIdx.x < groups) prefetch(blockIdx.x, 0);
+  int buf = 0;
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x, buf ^= 1) {
     const int64_t e = g * 32 + lane;
     const bool live = e < args.n_elem;
-    const int64_t ec = live ? e : args.n_elem - 1;
+    if (g + gridDim.x < groups) prefetch(g + gridDim.x, buf ^ 1);
+    else cp_async_commit();  // keep the group count uniform
+    cp_async_wait<1>();      // this group's copies have landed
+    double* sC = p2_smem + C::OFF_C + buf * 16 * 32;
     if (warp == 0) {
+      const double* sx = p2_smem + C::OFF_G + buf * 18 * 32 + lane;
       double x[18], d[21];
 #pragma unroll
-      for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+      for (int c = 0; c < 18; ++c) x[c] = sx[c * 32];
       prism_edges(x, d);
 #pragma unroll
       for (int c = 0; c < 21; ++c) sD[c * 32 + lane] = d[c];
-    } else if (GENERAL && warp == 1) {
+    } else if (GENERAL && warp == 1 && !args.coeff) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c) sC[c * 32 + lane] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
+      for (int c = 0; c < 16; ++c) sC[c * 32 + lane] = args.cu[c];
     }
     __syncthreads();
     // M for the 18 points (18 / NW per warp)
