@@ -13,8 +13,9 @@
  *    element) surface on pi_check() / any host-buffer call, reporting the
  *    LOWEST offending global element id, like integrate_generic would have
  *    thrown for it first (integrate_ref.cpp:72-75, kernels.cpp:158,249).
- *  - A context is bound to one device and one (p, n_eq); it is not
- *    thread-safe; use one per device / host thread.
+ *  - A context is bound to one device and one (p, n_eq), n_eq = 1 (scalar
+ *    weak forms) or 3 (systems: elasticity); it is not thread-safe; use one
+ *    per device / host thread.
  */
 #ifndef PRISM_B200_H
 #define PRISM_B200_H
@@ -61,7 +62,12 @@ enum {
 enum {
   PI_COEFF_LAPLACE = 0,     /* c[0][0][d][d] = 1, d = 1..3 (test_integrate_ref.cpp:72-75); coeff == NULL */
   PI_COEFF_UNIFORM = 1,     /* one HOST tensor [n_eq*n_eq*16] for every element */
-  PI_COEFF_PER_ELEMENT = 2  /* DEVICE SoA [n_eq*n_eq*16][ld]; entry k of element e at k*ld + e */
+  PI_COEFF_PER_ELEMENT = 2, /* DEVICE SoA [n_eq*n_eq*16][ld]; entry k of element e at k*ld + e */
+  /* n_eq = 3 isotropic linear elasticity, elasticity_tensor(MaterialData)
+   * (coefficients.cpp:40-59) -- the reference's model problem and the material
+   * input of its batch API (MaterialData per element, kernels.hpp:47-50): */
+  PI_COEFF_ELASTICITY = 3,  /* DEVICE SoA [2][ld]: (young_E, poisson_nu) of element e at e, ld + e */
+  PI_COEFF_ELASTICITY_UNIFORM = 4 /* HOST [2]: one (young_E, poisson_nu) for every element */
 };
 
 /* Kernel strategy selector (the role KernelVariant plays in planner.hpp:43-56). */

@@ -27,7 +27,7 @@ import numpy as np
 __all__ = [
     "Error", "ConfigError", "DomainError", "UnsupportedDegreeError", "InvertedElementError",
     "CapacityError", "SharedMemoryError", "ContractViolation", "IoError", "CudaError",
-    "LAPLACE", "UNIFORM", "PER_ELEMENT", "OUT_CANONICAL", "OUT_SOA",
+    "LAPLACE", "UNIFORM", "PER_ELEMENT", "ELASTICITY", "ELASTICITY_UNIFORM", "OUT_CANONICAL", "OUT_SOA",
     "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
     "generate_box_mesh", "generate_cdr_coefficients", "laplace_tensor",
@@ -38,6 +38,9 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libprism_b200.so"
 
 LAPLACE, UNIFORM, PER_ELEMENT = 0, 1, 2
+# n_eq = 3 isotropic elasticity from MaterialData (young_E, poisson_nu): per element
+# (device SoA [2][ld] / host AoS [n][2]) or one material for all elements (host [2]).
+ELASTICITY, ELASTICITY_UNIFORM = 3, 4
 OUT_CANONICAL, OUT_SOA = 0, 1
 VARIANT_AUTO, VARIANT_DENSE, VARIANT_SUMFACT = 0, 1, 2
 
@@ -328,14 +331,14 @@ class Integrator:
         """pi_integrate on device memory.  geom: SoA [18][geom_ld]; out: device buffer."""
         err = _ErrInfo()
         cbuf = None
-        if coeff_mode == UNIFORM:
+        if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
             cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
             caddr = cbuf.ctypes.data
         else:
-            caddr = _addr(coeff) if coeff_mode == PER_ELEMENT else None
+            caddr = _addr(coeff) if coeff_mode in (PER_ELEMENT, ELASTICITY) else None
         if geom_ld is None:
             geom_ld = geom.shape[1] if hasattr(geom, "shape") else n_elem
-        if coeff_ld is None and coeff_mode == PER_ELEMENT:
+        if coeff_ld is None and coeff_mode in (PER_ELEMENT, ELASTICITY):
             coeff_ld = coeff.shape[1] if hasattr(coeff, "shape") else n_elem
         st = library().pi_integrate(self._h, n_elem, element_id_base, _addr(geom) if not isinstance(geom, int) else geom,
                                     geom_ld, coeff_mode, caddr, coeff_ld or 0,
@@ -365,9 +368,9 @@ class Integrator:
         if out is None:
             out = np.empty((n, self.dim, self.dim))
         cbuf = None
-        if coeff_mode == UNIFORM:
+        if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
             cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
-        elif coeff_mode == PER_ELEMENT:
+        elif coeff_mode in (PER_ELEMENT, ELASTICITY):
             cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(n, -1)
         err = _ErrInfo()
         st = library().pi_integrate_host(self._h, n, element_id_base, _addr(geoms), coeff_mode, _addr(cbuf),

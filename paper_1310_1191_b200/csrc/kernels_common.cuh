@@ -16,7 +16,7 @@ struct LaunchArgs {
   int64_t geom_ld;
   const double* coeff;  // PER_ELEMENT: SoA [16][coeff_ld]; else nullptr
   int64_t coeff_ld;
-  double cu[16];        // UNIFORM coefficient tensor (GENERAL kernels)
+  double cu[144];       // UNIFORM coefficient tensor [n_eq][n_eq][4][4] (or E, nu)
   double* out;
   int out_layout;
   int64_t ld_out;
@@ -126,13 +126,13 @@ __device__ __forceinline__ void prism_edges(const double* __restrict__ x, double
 //            M_k0 = w sum_a c_a-1,k-1 C_a0,
 //            M_kl = (w/det) sum_ab c_a-1,k-1 C_ab c_b-1,l-1.
 // Returns det (<= 0 flags an inverted element, geometry.cpp:67-69).
-// DS / CS: element strides of the edge-vector and coefficient arrays (1 for
-// per-thread arrays; 32 for lane-interleaved shared-memory arrays).
-template <bool GENERAL, int DS = 1, int CS = 1>
-__device__ __forceinline__ double point_block(const double* __restrict__ dp, double xi1, double xi2, double xi3,
-                                              double w, const double* cp, double M[16]) {
+// Jacobian of the multilinear map at xi from the edge vectors (stride DS)
+// and its cofactors cf[i][k] (of J[i][k] = dx_i/dxi_k); returns det.
+// inv[k][i] = cf[i][k] / det (geometry.cpp:60-83).
+template <int DS = 1>
+__device__ __forceinline__ double jacobian_cofactors(const double* __restrict__ dp, double xi1, double xi2,
+                                                     double xi3, double cf[3][3]) {
   auto d = [dp](int i) { return dp[i * DS]; };
-  auto c = [cp](int i) { return cp[i * CS]; };
   const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
   const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
   double j[3][3];
@@ -142,7 +142,6 @@ __device__ __forceinline__ double point_block(const double* __restrict__ dp, dou
     j[i][1] = fma(zm, d(6 + i), zp * d(9 + i));
     j[i][2] = fma(l0, d(12 + i), fma(l1, d(15 + i), l2 * d(18 + i)));
   }
-  double cf[3][3];  // cf[i][k] = cofactor of J[i][k]
   cf[0][0] = j[1][1] * j[2][2] - j[1][2] * j[2][1];
   cf[0][1] = j[1][2] * j[2][0] - j[1][0] * j[2][2];
   cf[0][2] = j[1][0] * j[2][1] - j[1][1] * j[2][0];
@@ -152,8 +151,20 @@ __device__ __forceinline__ double point_block(const double* __restrict__ dp, dou
   cf[2][0] = j[0][1] * j[1][2] - j[0][2] * j[1][1];
   cf[2][1] = j[0][2] * j[1][0] - j[0][0] * j[1][2];
   cf[2][2] = j[0][0] * j[1][1] - j[0][1] * j[1][0];
-  const double det = j[0][0] * cf[0][0] + j[0][1] * cf[0][1] + j[0][2] * cf[0][2];
-  const double wd = w * __drcp_rn(det);
+  return j[0][0] * cf[0][0] + j[0][1] * cf[0][1] + j[0][2] * cf[0][2];
+}
+
+// The per-point block M = T (det w C) T^T of coefficient_block, built from
+// the cofactors c_ik of J without forming J^-1:
+//   Laplace  M_kl = (w/det) sum_i c_i,k-1 c_i,l-1            (k, l >= 1)
+//   general  M_00 = w det C_00,  M_0l = w sum_b C_0b c_b-1,l-1,
+//            M_k0 = w sum_a c_a-1,k-1 C_a0,
+//            M_kl = (w/det) sum_ab c_a-1,k-1 C_ab c_b-1,l-1.
+// wd = w / det.  CS: element stride of the coefficient array.
+template <bool GENERAL, int CS = 1>
+__device__ __forceinline__ void block_from_cofactors(const double cf[3][3], double det, double w, double wd,
+                                                     const double* cp, double M[16]) {
+  auto c = [cp](int i) { return cp[i * CS]; };
   if (!GENERAL) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -186,9 +197,41 @@ __device__ __forceinline__ double point_block(const double* __restrict__ dp, dou
         M[(k + 1) * 4 + (l + 1)] = wd * fma(cf[0][k], W[1][l], fma(cf[1][k], W[2][l], cf[2][k] * W[3][l]));
     }
   }
-  return det;
 }
 
+// Isotropic elasticity block (ie, je) (elasticity_tensor, coefficients.cpp:40-59:
+// c[ie][je][a+1][b+1] = lam d_(ie,a) d_(je,b) + mu d_(ie,je) d_ab + mu d_(ie,b) d_(je,a)):
+//   M_(k+1)(l+1) = (w/det) [lam c_ie,k c_je,l + mu c_je,k c_ie,l + mu d_(ie,je) sum_a c_a,k c_a,l]
+// (derivative rows/columns only; row/column 0 are not written).
+__device__ __forceinline__ void elasticity_block(const double cf[3][3], double wd, double lam, double mu, int ie,
+                                                 int je, double M[16]) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      double v = fma(lam * cf[ie][k], cf[je][l], mu * cf[je][k] * cf[ie][l]);
+      if (ie == je) v = fma(mu, fma(cf[0][k], cf[0][l], fma(cf[1][k], cf[1][l], cf[2][k] * cf[2][l])), v);
+      M[(k + 1) * 4 + (l + 1)] = wd * v;
+    }
+}
+
+// Lame parameters (lame_parameters, coefficients.cpp:28-37).
+__device__ __forceinline__ void lame(double young, double nu, double& lam, double& mu) {
+  mu = young / (2.0 * (1.0 + nu));
+  lam = young * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+}
+
+// DS / CS: element strides of the edge-vector and coefficient arrays (1 for
+// per-thread arrays; 32 for lane-interleaved shared-memory arrays).
+// Returns det (<= 0 flags an inverted element, geometry.cpp:67-69).
+template <bool GENERAL, int DS = 1, int CS = 1>
+__device__ __forceinline__ double point_block(const double* __restrict__ dp, double xi1, double xi2, double xi3,
+                                              double w, const double* cp, double M[16]) {
+  double cf[3][3];
+  const double det = jacobian_cofactors<DS>(dp, xi1, xi2, xi3, cf);
+  block_from_cofactors<GENERAL, CS>(cf, det, w, w * __drcp_rn(det), cp, M);
+  return det;
+}
 
 // ---- asynchronous global -> shared copies (cp.async, SASS LDGSTS) ----
 __device__ __forceinline__ void cp_async8(double* sdst, const double* gsrc) {

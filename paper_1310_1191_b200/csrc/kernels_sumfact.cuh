@@ -22,105 +22,155 @@
 //    computes exactly the B-fragment value G[k][j] its own m8n8k4 FP64 MMA
 //    consumes (3 FMAs from H and X in shared memory), so G never touches
 //    memory; the A fragments (X) are staged once per CTA in fragment order.
+//
+// Systems (n_eq = NE > 1, e.g. linear elasticity): the canonical row
+// i_dof*NE + i_e = (t*(p+1) + a)*NE + i_e = t*NVE + a' with the combined
+// vertical index a' = a*NE + i_e (NVE = NE*(p+1)), and likewise for columns.
+// The GEMM above is unchanged with (a, b) -> (a', b'); only H changes:
+//     H_xy(s,a',b') = sum_z sum_{k in x, l in y} Y_k(a,z) M^{ie,je}_kl(s,z) Y_l(b,z)
+// with one 4x4 block M^{ie,je} per equation pair and point.
 #pragma once
 
 #include "kernels_common.cuh"
 
 namespace pib {
 
+// Weak forms the kernel instantiates.
+enum SumFactForm {
+  kFormLaplace = 0,     // c[0][0][d][d] = 1 (derivative-only, built in)
+  kFormGeneral = 1,     // any element-constant tensor c[ie][je][4][4]
+  kFormElasticity = 2   // isotropic elasticity from (E, nu) per element (coefficients.cpp:23-59)
+};
+
 // Column order of a K row block inside the GEMM ("n-tiles" of 8 columns):
 //  natural: n-tile nt = columns j = 8 nt .. 8 nt + 7, j = t'*(p+1) + b;
 //  t'-major (TMAJOR): n-tile (g, b) = columns t' = 8g .. 8g+7 at fixed b, so
 //  a lane's X values are shared by every b-tile and H is warp-uniform per
 //  tile (the better order when p+1 does not divide 8).
-template <int P, bool TMAJOR>
+template <int P, int NE, bool TMAJOR>
 struct SumFactShape {
   static constexpr int NV = P + 1;                    // Legendre modes / GL points
   static constexpr int NZ = P + 1;
+  static constexpr int NVE = NE * NV;                 // combined vertical index a' = a*NE + ie
   static constexpr int NT = (P + 1) * (P + 2) / 2;    // triangle monomials
   static constexpr int NS = (P == 1 ? 3 : P == 2 ? 6 : P == 3 ? 12 : P == 4 ? 16 : P == 5 ? 25 : P == 6 ? 33 : 42);
   static constexpr int NSP = (NS + 3) / 4 * 4;        // padded to whole chunks
-  static constexpr int NSH = NT * NV;
+  static constexpr int NSH = NT * NVE;                // K dimension (n_eq * shape_count)
   static constexpr int NQ = NS * NZ;
   static constexpr int MT = (NT + 7) / 8;             // m-tiles of the X operand (rows t)
-  static constexpr int NTILE = TMAJOR ? MT * NV : (NSH + 7) / 8;
-  static constexpr int NTP = TMAJOR ? MT * 8 : (NTILE * 8 + NV - 1) / NV;  // t' rows of the X table
   static constexpr int KSTEPS = 3 * NSP / 4;          // k4-steps over (s, x)
   static constexpr int NCHUNK = NSP / 4;              // 4 triangle points per chunk
   static constexpr int XFRAG = MT * KSTEPS * 32;      // doubles in the A-fragment table
+};
+
+// Launch shape: EPC elements x AG vertical rows a' per CTA; each consumer
+// warp owns WA rows a' x NB n-tiles x all MT m-tiles (WA*NB*MT fragments);
+// NPW producer warps; NCB column blocks (CTAs) per (element, a'-group).
+// TMAJOR warps own NG t'-groups x NBB b values (NB = NG*NBB).
+template <int P, int NE>
+struct SumFactLaunch;
+template <> struct SumFactLaunch<2, 1> {
+  static constexpr bool TMAJOR = true;
+  static constexpr int EPC = 8, AG = 3, WA = 3, NG = 1, NBB = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<3, 1> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 2, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 1, MINB = 2, NCB = 1;
+};
+template <> struct SumFactLaunch<4, 1> {
+  static constexpr bool TMAJOR = true;
+  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 3, BSPLIT = 1, MINB = 2, NCB = 1;
+};
+template <> struct SumFactLaunch<5, 1> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<6, 1> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<7, 1> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1, NCB = 1;
+};
+// n_eq = 3 (elasticity): K is 9x larger; p >= 6 also splits columns over CTAs.
+template <> struct SumFactLaunch<1, 3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 2, AG = 6, WA = 3, NG = 0, NBB = 0, NB = 3, NPW = 2, BSPLIT = 2, MINB = 2, NCB = 1;
+};
+template <> struct SumFactLaunch<2, 3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 9, WA = 3, NG = 0, NBB = 0, NB = 7, NPW = 2, BSPLIT = 3, MINB = 2, NCB = 1;
+};
+template <> struct SumFactLaunch<3, 3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 3, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<4, 3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 10, NPW = 3, BSPLIT = 5, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<5, 3> {
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 6, MINB = 1, NCB = 1;
+};
+template <> struct SumFactLaunch<6, 3> {  // column blocks of 42 tiles = 16 t' rows
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 6, NPW = 2, BSPLIT = 7, MINB = 1, NCB = 2;
+};
+template <> struct SumFactLaunch<7, 3> {  // column blocks of 36 tiles = 12 t' rows
+  static constexpr bool TMAJOR = false;
+  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 8, MINB = 1, NCB = 3;
+};
+
+template <int P, int NE = 1>
+struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFactLaunch<P, NE> {
+  using S = SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>;
+  using L = SumFactLaunch<P, NE>;
+  // n-tiles of 8 columns: t'-major (g, b') tiles, or natural tiles padded to
+  // a whole number of NB x NCB blocks (padding columns are computed from
+  // zero X rows and never stored)
+  static constexpr int NTILE = L::TMAJOR ? S::MT * S::NVE : ((S::NSH + 7) / 8 + L::NB * L::NCB - 1) / (L::NB * L::NCB) * (L::NB * L::NCB);
+  static constexpr int NTP = L::TMAJOR ? S::MT * 8 : (NTILE * 8 + S::NVE - 1) / S::NVE;  // t' rows of the X table
   // X as [s][y][t'] with a row pitch NTPS = NTP rounded up to 8 (mod 16):
   // rows s and s+1 then start 64 bytes apart modulo 128, so the two s a
   // warp reads per k-step land in disjoint bank halves.
   static constexpr int NTPS = (NTP + 7) / 16 * 16 + 8;
-  static constexpr int XPLAIN = NSP * 3 * NTPS;
-};
-
-// Launch shape: EPC elements x AG Legendre rows `a` per CTA; each consumer
-// warp owns WA rows a x NB n-tiles x all MT m-tiles (WA*NB*MT fragments);
-// NPW producer warps.  TMAJOR warps own NG t'-groups x NBB b values (NB = NG*NBB).
-template <int P>
-struct SumFactLaunch;
-template <> struct SumFactLaunch<2> {
-  static constexpr bool TMAJOR = true;
-  static constexpr int EPC = 8, AG = 3, WA = 3, NG = 1, NBB = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 1;
-};
-template <> struct SumFactLaunch<3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 2, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 1, MINB = 2;
-};
-template <> struct SumFactLaunch<4> {
-  static constexpr bool TMAJOR = true;
-  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 3, BSPLIT = 1, MINB = 2;
-};
-template <> struct SumFactLaunch<5> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1;
-};
-template <> struct SumFactLaunch<6> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1;
-};
-template <> struct SumFactLaunch<7> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1;
-};
-
-template <int P>
-struct SumFactConfig : SumFactShape<P, SumFactLaunch<P>::TMAJOR>, SumFactLaunch<P> {
-  using S = SumFactShape<P, SumFactLaunch<P>::TMAJOR>;
-  using L = SumFactLaunch<P>;
-  static constexpr int NBLK = S::NTILE / L::NB;
-  static constexpr int WPE = (L::AG / L::WA) * NBLK;   // consumer warps per element
+  static constexpr int XPLAIN = S::NSP * 3 * NTPS;
+  static constexpr int NBLK = NTILE / (L::NB * L::NCB);  // n-tile blocks (warps) per CTA and row group
+  static constexpr int WPE = (L::AG / L::WA) * NBLK;      // consumer warps per element
   // t'-major warps own whole K rows (all t'-groups, all b), so they stage
   // and store their rows without CTA-level synchronisation.
-  static_assert(!L::TMAJOR || (L::NB == L::NG * L::NBB && L::NG == S::MT && L::NBB == S::NV),
+  static_assert(!L::TMAJOR || (L::NB == L::NG * L::NBB && L::NG == S::MT && L::NBB == S::NVE && L::NCB == 1),
                 "t'-major warp tiling");
   static constexpr int NCW = L::EPC * WPE;
   static constexpr int NWARPS = NCW + L::NPW;
   static constexpr int NTHREADS = 32 * NWARPS;
   static constexpr int NPT = 32 * L::NPW;              // producer threads
-  static constexpr int NAG = S::NV / L::AG;            // CTAs per element group
-  static constexpr int BPER = (S::NV + L::BSPLIT - 1) / L::BSPLIT;  // b values per H item
-  // Along a consumer lane's n-tiles, b = (8*nb + lane/4) mod NV repeats with
-  // period R = NV / gcd(8, NV); its H values are cached in registers.
-  static constexpr int R = S::NV / (S::NV % 8 == 0 ? 8 : S::NV % 4 == 0 ? 4 : S::NV % 2 == 0 ? 2 : 1);
-  static constexpr int RC = R < L::NB ? R : L::NB;     // distinct b values a lane touches
-  static_assert(S::NV % L::AG == 0 && L::AG % L::WA == 0, "bad a-grouping");
-  static_assert(S::NTILE % L::NB == 0, "n-tiles must split evenly");
-  // H for one chunk: [EPC][AG][4 s][NV b][3 x][4 y (padded)]
-  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NV * 12;
+  static constexpr int NAG = S::NVE / L::AG;           // a'-groups per element
+  static constexpr int NITEM = NAG * L::NCB;           // CTA work items per element group
+  static constexpr int BPER = (S::NVE + L::BSPLIT - 1) / L::BSPLIT;  // b' values per H item
+  // Along a consumer lane's n-tiles, b' = (8*nb + lane/4) mod NVE repeats with
+  // period R = NVE / gcd(8, NVE); its H values are cached in registers.
+  static constexpr int R = S::NVE / (S::NVE % 8 == 0 ? 8 : S::NVE % 4 == 0 ? 4 : S::NVE % 2 == 0 ? 2 : 1);
+  static constexpr int RC = R < L::NB ? R : L::NB;     // distinct b' values a lane touches
+  static_assert(S::NVE % L::AG == 0 && L::AG % L::WA == 0, "bad a-grouping");
+  static_assert(NTILE % (L::NB * L::NCB) == 0, "n-tiles must split evenly");
+  // H for one chunk: [EPC][AG][4 s][NVE b'][3 x][4 y (padded)]
+  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NVE * 12;
   static constexpr int NBUF = 3;  // H ring depth (producers run up to NBUF chunks ahead)
   static constexpr int MITEMS = L::EPC * 4 * S::NZ;   // points per chunk
-  static constexpr int MPITCH = MITEMS | 1;             // M stored k-major: [16][MPITCH]
-  static constexpr int M_PER_CHUNK = 16 * MPITCH;
+  static constexpr int MPITCH = MITEMS | 1;             // M stored k-major: [NE*NE][16][MPITCH]
+  static constexpr int M_PER_CHUNK = NE * NE * 16 * MPITCH;
+  static constexpr int NCOEF = 16 * NE * NE;            // coefficient tensor per element
   // shared memory layout (doubles; every block 16-byte aligned)
   static constexpr int OFF_XA = 0;
   static constexpr int OFF_XP = OFF_XA + S::XFRAG;
-  static constexpr int OFF_H = OFF_XP + S::XPLAIN;
+  static constexpr int OFF_H = OFF_XP + XPLAIN;
   static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
   static constexpr int OFF_GEOM = OFF_M + M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + (L::EPC * 21 + 1) / 2 * 2;
-  static constexpr int OFF_LINE = OFF_C + L::EPC * 16;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
+  static constexpr int OFF_LINE = OFF_C + L::EPC * NCOEF;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
   static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
   // t'-major epilogue: each consumer warp stages its WA*NT K rows
@@ -156,17 +206,19 @@ constexpr int kBarFull0 = 1, kBarEmpty0 = 4, kBarProd = 7, kBarCons = 8;  // FUL
 // Release fence for the shared-memory hand-off before bar.arrive (MEMBAR.ALL.CTA).
 __device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
 
-// SYM: the coefficient tensor is symmetric, so K is.  Where a CTA holds all
-// rows of an element (t'-major, NAG == 1) only the blocks with t'-block >=
-// t-block are multiplied; the rest are mirrored from the CTA's staged K.
-template <int P, bool GENERAL, bool SYM>
-__global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::MINB)
+// FORM: SumFactForm.  SYM: the coefficient tensor is symmetric, so K is.
+// Where a CTA holds all rows of an element (t'-major, NAG == 1) only the
+// blocks with t'-block >= t-block are multiplied; the rest are mirrored
+// from the CTA's staged K.
+template <int P, int NE, int FORM, bool SYM>
+__global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<P, NE>::MINB)
     sumfact_kernel(LaunchArgs args, SumFactTables tab) {
-  using C = SumFactConfig<P>;
+  using C = SumFactConfig<P, NE>;
+  constexpr bool GENERAL = FORM == kFormGeneral;  // value row/column present in M
   constexpr bool SYMK = SYM && C::TMAJOR && C::NAG == 1;
-  constexpr int NV = C::NV, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ, NTPS = C::NTPS;
-  constexpr int MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
-  constexpr int NCHUNK = C::NCHUNK;
+  constexpr int NV = C::NV, NVE = C::NVE, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ;
+  constexpr int NTPS = C::NTPS, MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
+  constexpr int NCHUNK = C::NCHUNK, NCOEF = C::NCOEF;
   extern __shared__ __align__(16) double smem[];
   double* sXA = smem + C::OFF_XA;
   double* sXP = smem + C::OFF_XP;
@@ -191,8 +243,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   const double* Pv = sY;            // P_a(z)  [NZ][NV]
   const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]
 
-  // Work items: (element group, a-group); this CTA takes items blockIdx.x + k*gridDim.x.
-  const int64_t n_items = (args.n_elem + EPC - 1) / EPC * C::NAG;
+  // Work items: (element group, a'-group, column block); this CTA takes
+  // items blockIdx.x + k*gridDim.x.
+  const int64_t n_items = (args.n_elem + EPC - 1) / EPC * C::NITEM;
   const int64_t my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t total_chunks = my_items * NCHUNK;
 
@@ -202,8 +255,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     int64_t gc = 0;  // chunk counter across items: selects the H buffer
     for (int64_t it = 0; it < my_items; ++it) {
       const int64_t w = blockIdx.x + it * gridDim.x;
-      const int64_t e0 = (w / C::NAG) * EPC;
-      const int agroup = static_cast<int>(w % C::NAG);
+      const int64_t e0 = (w / C::NITEM) * EPC;
+      const int agroup = static_cast<int>((w % C::NITEM) / C::NCB);
+      const bool flagger = (w % C::NITEM) == 0;  // one item per element group reports inversions
       if (ptid < EPC) {  // edge vectors of the item's elements
         const int64_t e = e0 + ptid;
         const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;  // pad with a valid element
@@ -214,42 +268,61 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
         for (int c = 0; c < 21; ++c) sGeom[ptid * 21 + c] = d[c];
       }
-      if (GENERAL) {
-        for (int i = ptid; i < EPC * 16; i += C::NPT) {
-          const int el = i / 16, c = i % 16;
+      if (FORM == kFormGeneral) {
+        for (int i = ptid; i < EPC * NCOEF; i += C::NPT) {
+          const int el = i / NCOEF, c = i % NCOEF;
           const int64_t e = e0 + el;
           const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;
           sC[i] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
         }
+      } else if (FORM == kFormElasticity) {
+        if (ptid < EPC) {  // Lame parameters from (E, nu)
+          const int64_t e = e0 + ptid;
+          const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;
+          const double young = args.coeff ? args.coeff[ec] : args.cu[0];
+          const double nu = args.coeff ? args.coeff[args.coeff_ld + ec] : args.cu[1];
+          lame(young, nu, sC[2 * ptid], sC[2 * ptid + 1]);
+        }
       }
       named_sync(kBarProd, C::NPT);
       for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
-        // (1) M for the chunk's points: (el, sl, z)
+        // (1) M blocks for the chunk's points: (el, sl, z)
         for (int i = ptid; i < EPC * 4 * NZ; i += C::NPT) {
           const int z = i % NZ, sl = (i / NZ) % 4, el = i / (4 * NZ);
           const int s = chunk * 4 + sl;
-          double M[16];
+          double* Mi = sM + i;
           if (s < NS) {
-            const double det = point_block<GENERAL>(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z],
-                                                    sW[z * NS + s], sC + 16 * el, M);
+            double cf[3][3];
+            const double det = jacobian_cofactors(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
+            const double w8 = sW[z * NS + s], wd = w8 * __drcp_rn(det);
             const int64_t e = e0 + el;
-            if (!(det > 0.0) && e < args.n_elem && agroup == 0) flag_inverted(args.bad, args.element_id_base + e);
+            if (!(det > 0.0) && e < args.n_elem && flagger) flag_inverted(args.bad, args.element_id_base + e);
+#pragma unroll
+            for (int blk = 0; blk < NE * NE; ++blk) {
+              double M[16];
+              if (FORM == kFormElasticity)
+                elasticity_block(cf, wd, sC[2 * el], sC[2 * el + 1], blk / NE, blk % NE, M);
+              else
+                block_from_cofactors<GENERAL>(cf, det, w8, wd, sC + NCOEF * el + 16 * blk, M);
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                if (GENERAL || (k >= 4 && (k & 3) != 0)) Mi[(blk * 16 + k) * C::MPITCH] = M[k];
+            }
           } else {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) M[k] = 0.0;
+            for (int k = 0; k < 16 * NE * NE; ++k) Mi[k * C::MPITCH] = 0.0;
           }
-#pragma unroll
-          for (int k = 0; k < 16; ++k) sM[k * C::MPITCH + i] = M[k];
         }
         named_sync(kBarProd, C::NPT);
         const int buf = static_cast<int>(gc % C::NBUF);
         if (gc >= C::NBUF) named_sync(kBarEmpty0 + buf, C::NTHREADS);  // consumers released this buffer
         double* Hb = sH + buf * C::H_PER_BUF;
-        // (2) H_x,y(s,a,b), y = 0..2: items (el, al, sl, x, b-group), b looped
+        // (2) H_x,y(s,a',b'), y = 0..2: items (el, al, sl, x, b'-group), b' looped
         for (int i = ptid; i < EPC * AG * 4 * 3 * C::BSPLIT; i += C::NPT) {
           const int bg = i % C::BSPLIT, x = (i / C::BSPLIT) % 3, sl = (i / (3 * C::BSPLIT)) % 4;
           const int al = (i / (12 * C::BSPLIT)) % AG, el = i / (12 * C::BSPLIT * AG);
-          const int a = agroup * AG + al;
+          const int ap = agroup * AG + al;          // a' = a*NE + ie
+          const int a = ap / NE, ie = ap % NE;
           const int kx = x < 2 ? x + 1 : 3;
           double h[C::BPER][3];
 #pragma unroll
@@ -258,20 +331,21 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const double* Mz = Mp + z;
-            auto M = [Mz](int k) { return Mz[k * C::MPITCH]; };
             const double pa = Pv[z * NV + a], da = Pd[z * NV + a];
             // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
             // plus row 0 weighted by P for x = 2 in the general case)
             const double wr = x < 2 ? pa : da;
             const double w0 = (GENERAL && x == 2) ? pa : 0.0;
-            const double L0 = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
-            const double L1 = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
-            const double L2 = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
-            const double L3 = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
 #pragma unroll
             for (int bb = 0; bb < C::BPER; ++bb) {
-              const int b = bg * C::BPER + bb;
-              if (b < NV) {
+              const int bp = bg * C::BPER + bb;      // b' = b*NE + je
+              if (bp < NVE) {
+                const int b = bp / NE, je = bp % NE;
+                auto M = [Mz, ie, je](int k) { return Mz[((ie * NE + je) * 16 + k) * C::MPITCH]; };
+                const double L0 = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
+                const double L1 = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
+                const double L2 = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
+                const double L3 = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
                 const double pb = Pv[z * NV + b], db = Pd[z * NV + b];
                 h[bb][0] = fma(L1, pb, h[bb][0]);
                 h[bb][1] = fma(L2, pb, h[bb][1]);
@@ -281,9 +355,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           }
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) {
-            const int b = bg * C::BPER + bb;
-            if (b < NV) {
-              double* dst = Hb + ((((el * AG + al) * 4 + sl) * NV + b) * 3 + x) * 4;
+            const int bp = bg * C::BPER + bb;
+            if (bp < NVE) {
+              double* dst = Hb + ((((el * AG + al) * 4 + sl) * NVE + bp) * 3 + x) * 4;
               *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
               dst[2] = h[bb][2];
             }
@@ -300,7 +374,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
   // ======================= consumer warps =======================
   const int el_w = warp / C::WPE;
   const int r_w = warp % C::WPE;
-  const int al0 = (r_w / C::NBLK) * WA;  // first local a of this warp
+  const int al0 = (r_w / C::NBLK) * WA;  // first local a' of this warp
   const int nblk = r_w % C::NBLK;
   const int cpos = lane >> 2;            // B-fragment column within an n-tile
   const int64_t kk_elem = static_cast<int64_t>(NSH) * NSH;
@@ -313,24 +387,27 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
     sl_k[ks] = kk / 3;
     x_k[ks] = kk % 3;
   }
-  // Natural order: the warp's n-tiles.  With a symmetric tensor the tiles
-  // entirely below the t-block diagonal are skipped, so tiles are dealt to
-  // warps zig-zag (or strided, when the H register cache needs a fixed b
-  // period) to balance the remaining work.
-  constexpr bool SYMN = SYM && !C::TMAJOR && C::NAG == 1;  // mirrors stay inside the CTA's element
-  int ntl[NB], hoff[NB], xoff[NB];
+  // Natural order: the warp's n-tiles (of its column block, set per item).
+  // With a symmetric tensor the tiles entirely below the t-block diagonal
+  // are skipped, so tiles are dealt to warps zig-zag (or strided, when the
+  // H register cache needs a fixed b' period) to balance the remaining work.
+  constexpr bool SYMN = SYM && !C::TMAJOR && C::NAG == 1 && C::NCB == 1;  // mirrors stay inside the CTA's element
+  constexpr int NTB = C::NTILE / C::NCB;  // n-tiles per column block
+  int ntl0[NB], hoff[NB], xoff0[NB];
   unsigned need[NB];
   if constexpr (!C::TMAJOR) {
     constexpr bool ZIGZAG = (C::R == 1) || (C::RC == NB);
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
-      ntl[nb] = SYMN ? (ZIGZAG ? nb * C::NBLK + ((nb & 1) ? C::NBLK - 1 - nblk : nblk) : nb * C::NBLK + nblk)
-                     : nblk * NB + nb;
-      const int j = ntl[nb] * 8 + cpos;
-      const int tp = j / NV, b = j - tp * NV;
+      ntl0[nb] = SYMN ? (ZIGZAG ? nb * C::NBLK + ((nb & 1) ? C::NBLK - 1 - nblk : nblk) : nb * C::NBLK + nblk)
+                      : nblk * NB + nb;
+      // column j = (cb*NTB + ntl0)*8 + cpos; NTB*8 is a multiple of NVE only
+      // when NCB == 1, so b' and t' are resolved per item below for NCB > 1.
+      const int j = ntl0[nb] * 8 + cpos;
+      const int tp = j / NVE, b = j - tp * NVE;
       hoff[nb] = b * 12;  // + x*4 at use
-      xoff[nb] = tp;      // + s*3*NTPS at use
-      const int tmax = min(NT - 1, (ntl[nb] * 8 + 7) / NV);
+      xoff0[nb] = tp;     // + s*3*NTPS at use
+      const int tmax = min(NT - 1, (ntl0[nb] * 8 + 7) / NVE);
       unsigned m = 0;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -338,6 +415,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
       need[nb] = m;
     }
   }
+  static_assert(C::NCB == 1 || (NTB * 8) % NVE == 0, "column blocks must start at a t' boundary");
 
   int64_t gc = 0;
   for (int64_t it = 0; it <= my_items; ++it) {
@@ -346,8 +424,13 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
       break;
     }
     const int64_t w = blockIdx.x + it * gridDim.x;
-    const int64_t e = (w / C::NAG) * EPC + el_w;
-    const int agroup = static_cast<int>(w % C::NAG);
+    const int64_t e = (w / C::NITEM) * EPC + el_w;
+    const int agroup = static_cast<int>((w % C::NITEM) / C::NCB);
+    const int cb = static_cast<int>(w % C::NCB);
+    const int tp_cb = cb * (NTB * 8 / NVE);  // first t' of the column block
+    int xoff[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) xoff[nb] = xoff0[nb] + tp_cb;
 
     double acc[WA][MT][NB][2];
 #pragma unroll
@@ -373,7 +456,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
         const double* afr = afr3[ks];
         const int s = chunk * 4 + sl_k[ks];
         if constexpr (C::TMAJOR) {
-          // n-tile (g, b): columns t' = 8g + cpos at fixed b; lane's X shared by all b
+          // n-tile (g, b'): columns t' = 8g + cpos at fixed b'; lane's X shared by all b'
           double xv[MT][3];
 #pragma unroll
           for (int g = 0; g < MT; ++g) {
@@ -384,9 +467,9 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + ((((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 3 + x_k[ks]) * 4;
+            const double* Hs = Hb + ((((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NVE) * 3 + x_k[ks]) * 4;
 #pragma unroll
-            for (int b = 0; b < NV; ++b) {
+            for (int b = 0; b < NVE; ++b) {
               const double2 h01 = *reinterpret_cast<const double2*>(Hs + b * 12);
               const double h2 = Hs[b * 12 + 2];
 #pragma unroll
@@ -394,13 +477,13 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
-                  if (!SYMK || g >= mt) dmma_8x8x4(acc[wa][mt][g * NV + b][0], acc[wa][mt][g * NV + b][1], afr[mt], gv);
+                  if (!SYMK || g >= mt) dmma_8x8x4(acc[wa][mt][g * NVE + b][0], acc[wa][mt][g * NVE + b][1], afr[mt], gv);
               }
             }
           }
         } else {
           const double* Xs = sXP + s * 3 * NTPS;
-          // X values of the lane's n-tiles, shared by the WA rows a
+          // X values of the lane's n-tiles, shared by the WA rows a'
           double xr[WA > 1 ? NB : 1][3];
           if constexpr (WA > 1) {
 #pragma unroll
@@ -413,8 +496,8 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NV) * 12 + x_k[ks] * 4;
-            // b for n-tile nb is b_(nb mod R): load each distinct one once
+            const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NVE) * 12 + x_k[ks] * 4;
+            // b' for n-tile nb is b'_(nb mod R): load each distinct one once
             double hr[C::RC][3];
 #pragma unroll
             for (int m = 0; m < C::RC; ++m) {
@@ -457,18 +540,18 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t = mt * 8 + (lane >> 2);
-          const int row = t * NV + al0 + wa;
+          const int row = t * NVE + al0 + wa;
 #pragma unroll
           for (int g = SYMK ? mt : 0; g < MT; ++g)
 #pragma unroll
-            for (int b = 0; b < NV; ++b)
+            for (int b = 0; b < NVE; ++b)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int tp = g * 8 + 2 * (lane & 3) + h;
                 if (t < NT && tp < NT) {
-                  const double v = acc[wa][mt][g * NV + b][h];
-                  st[row * NSH + tp * NV + b] = v;
-                  if (SYMK && g > mt) st[(tp * NV + b) * NSH + row] = v;  // mirror of the skipped block
+                  const double v = acc[wa][mt][g * NVE + b][h];
+                  st[row * NSH + tp * NVE + b] = v;
+                  if (SYMK && g > mt) st[(tp * NVE + b) * NSH + row] = v;  // mirror of the skipped block
                 }
               }
         }
@@ -476,7 +559,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
       named_sync(kBarCons, 32 * C::NCW);
       if (bulk) {
         if (tid < EPC) {
-          const int64_t ee = (w / C::NAG) * EPC + tid;
+          const int64_t ee = (w / C::NITEM) * EPC + tid;
           if (ee < args.n_elem) {
             const double* src = smem + C::OFF_STAGE + tid * C::ESTRIDE + static_cast<int>((ee * kk_elem) & 1);
             bulk_store_doubles(args.out + ee * kk_elem, src, static_cast<int>(kk_elem));
@@ -485,7 +568,7 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
         }
       } else {
         for (int el = 0; el < EPC; ++el) {
-          const int64_t ee = (w / C::NAG) * EPC + el;
+          const int64_t ee = (w / C::NITEM) * EPC + el;
           if (ee >= args.n_elem) break;
           const double* src = smem + C::OFF_STAGE + el * C::ESTRIDE;
           for (int i = tid; i < kk_elem; i += 32 * C::NCW) {
@@ -510,15 +593,15 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
           for (int g = 0; g < MT; ++g)
 #pragma unroll
-            for (int b = 0; b < NV; ++b)
+            for (int b = 0; b < NVE; ++b)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int tp = g * 8 + 2 * (lane & 3) + h;
-                if (t < NT && tp < NT) st[(wa * NT + t) * NSH + tp * NV + b] = acc[wa][mt][g * NV + b][h];
+                if (t < NT && tp < NT) st[(wa * NT + t) * NSH + tp * NVE + b] = acc[wa][mt][g * NVE + b][h];
               }
         }
       __syncwarp();
-      const int64_t row0 = agroup * AG + al0;  // row of (t = 0, wa = 0); row(t, wa) = row0 + t*NV + wa
+      const int64_t row0 = agroup * AG + al0;  // row of (t = 0, wa = 0); row(t, wa) = row0 + t*NVE + wa
       if (args.out_layout == PI_OUT_CANONICAL) {
         double* dst = args.out + e * kk_elem + row0 * NSH;
 #pragma unroll
@@ -527,11 +610,11 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
           for (int t = 0; t < NT; ++t)
 #pragma unroll
             for (int j0 = 0; j0 < NSH; j0 += 32)
-              if (j0 + lane < NSH) dst[(t * NV + wa) * NSH + j0 + lane] = st[(wa * NT + t) * NSH + j0 + lane];
+              if (j0 + lane < NSH) dst[(t * NVE + wa) * NSH + j0 + lane] = st[(wa * NT + t) * NSH + j0 + lane];
       } else {
         for (int r = 0; r < WA * NT; ++r) {
           const int wa = r / NT, t = r % NT;
-          const int64_t row = row0 + t * NV + wa;
+          const int64_t row = row0 + t * NVE + wa;
           for (int j = lane; j < NSH; j += 32) args.out[(row * NSH + j) * args.ld_out + e] = st[r * NSH + j];
         }
       }
@@ -542,12 +625,12 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
           const int t = mt * 8 + (lane >> 2);
-          const int row = t * NV + agroup * AG + al0 + wa;
+          const int row = t * NVE + agroup * AG + al0 + wa;
 #pragma unroll
           for (int nb = 0; nb < NB; ++nb) {
             if (SYMN && !((need[nb] >> mt) & 1u)) continue;  // filled by the transposed tile's mirror
             if (t >= NT) continue;
-            const int j = ntl[nb] * 8 + 2 * (lane & 3);
+            const int j = (cb * NTB + ntl0[nb]) * 8 + 2 * (lane & 3);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int jj = j + h;
@@ -555,10 +638,10 @@ __global__ void __launch_bounds__(SumFactConfig<P>::NTHREADS, SumFactConfig<P>::
               const double v = acc[wa][mt][nb][h];
               bool mirror = false;
               if (SYMN) {
-                // the transposed entry (jj, row) sits in tile (m-tile of t' = jj/NV, n-tile of row);
+                // the transposed entry (jj, row) sits in tile (m-tile of t' = jj/NVE, n-tile of row);
                 // write it here when that tile is skipped
-                const int mt2 = (jj / NV) >> 3;
-                const int tmax2 = min(NT - 1, ((row >> 3) * 8 + 7) / NV);
+                const int mt2 = (jj / NVE) >> 3;
+                const int tmax2 = min(NT - 1, ((row >> 3) * 8 + 7) / NVE);
                 mirror = tmax2 < 8 * mt2;
               }
               if (args.out_layout == PI_OUT_CANONICAL) {

@@ -11,6 +11,7 @@
 #include "kernels_dense.cuh"
 #include "kernels_p2.cuh"
 #include "kernels_sumfact.cuh"
+#include "sumfact_api.hpp"
 #include "pi_internal.hpp"
 
 using namespace pib;
@@ -62,148 +63,6 @@ __global__ void aos_to_soa_kernel(const double* __restrict__ in, double* __restr
   out[c * ld + e] = in[i];
 }
 
-template <int P>
-struct SumFactHost {
-  using C = SumFactConfig<P>;
-  static void set_attrs() {
-    cudaFuncSetAttribute(sumfact_kernel<P, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM_BYTES));
-    cudaFuncSetAttribute(sumfact_kernel<P, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM_BYTES));
-    cudaFuncSetAttribute(sumfact_kernel<P, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM_BYTES));
-  }
-  // Persistent grid: as many CTAs as fit on the device at once (queried per
-  // instantiation), each looping over (element group, a-group) work items.
-  template <bool G, bool Y>
-  static int resident_ctas() {
-    static int c = 0;
-    if (c == 0) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, G, Y>, C::NTHREADS, C::SMEM_BYTES);
-      c = std::max(1, sms * std::max(1, per_sm));
-    }
-    return c;
-  }
-  template <bool G, bool Y>
-  static void go(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
-    const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NAG;
-    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<G, Y>())));
-    sumfact_kernel<P, G, Y><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
-  }
-  // general: full 4x4 tensor; symmetric: the tensor (hence K) is symmetric.
-  static void launch(const LaunchArgs& a, const SumFactTables& t, bool general, bool symmetric, cudaStream_t s) {
-    if (!general)
-      go<false, true>(a, t, s);
-    else if (symmetric)
-      go<true, true>(a, t, s);
-    else
-      go<true, false>(a, t, s);
-  }
-  // Builds the X fragment table, Y table and rule coordinates from the
-  // caller's rule and shape table; false if the table is not the tensor
-  // product the kernel factorises.
-  static bool build(pi_context* ctx, std::vector<double>& xfrag, std::vector<double>& xplain,
-                    std::vector<double>& yline, std::vector<double>& tri) {
-    constexpr int NS = C::NS, NZ = C::NZ, NV = C::NV, NT = C::NT, NSH = C::NSH;
-    if (ctx->n_q != NS * NZ || ctx->n_shape != NSH) return false;
-    const double* pts = ctx->h_pts.data();
-    const double* phi = ctx->h_phi.data();
-    auto PHI = [&](int q, int k, int dof) { return phi[(static_cast<size_t>(q) * 4 + k) * NSH + dof]; };
-    for (int z = 0; z < NZ; ++z)
-      for (int s = 0; s < NS; ++s) {
-        const int q = z * NS + s;
-        if (pts[3 * q] != pts[3 * s] || pts[3 * q + 1] != pts[3 * s + 1] || pts[3 * q + 2] != pts[3 * z * NS + 2])
-          return false;
-      }
-    tri.assign(2 * NS, 0.0);
-    for (int s = 0; s < NS; ++s) {
-      tri[s] = pts[3 * s];
-      tri[NS + s] = pts[3 * s + 1];
-    }
-    // Y: P_a(z) = phi_0((t=0,a), (s=0,z)), P'_a(z) = phi_3((0,a),(0,z)) since m_0 = 1.
-    yline.assign(2 * NV * NZ + NZ, 0.0);
-    for (int a = 0; a < NV; ++a)
-      for (int z = 0; z < NZ; ++z) {
-        yline[z * NV + a] = PHI(z * NS, 0, a);
-        yline[NV * NZ + z * NV + a] = PHI(z * NS, 3, a);
-      }
-    for (int z = 0; z < NZ; ++z) yline[2 * NV * NZ + z] = pts[3 * z * NS + 2];
-    // X_x(t,s): x=0 dm/dxi1, 1 dm/dxi2, 2 m, read at a=0 (P_0 = 1), z=0.
-    std::vector<double> X(static_cast<size_t>(3) * NT * NS);
-    for (int t = 0; t < NT; ++t)
-      for (int s = 0; s < NS; ++s) {
-        X[(0 * NT + t) * NS + s] = PHI(s, 1, t * NV);
-        X[(1 * NT + t) * NS + s] = PHI(s, 2, t * NV);
-        X[(2 * NT + t) * NS + s] = PHI(s, 0, t * NV) / PHI(s, 0, 0);
-      }
-    // Structure check: phi_k(i,q) == X(t,s) Y(a,z) to rounding.
-    double worst = 0.0, scale = 0.0;
-    for (int z = 0; z < NZ; ++z)
-      for (int s = 0; s < NS; ++s)
-        for (int t = 0; t < NT; ++t)
-          for (int a = 0; a < NV; ++a) {
-            const int q = z * NS + s, dof = t * NV + a;
-            const double Pz = yline[z * NV + a], D = yline[NV * NZ + z * NV + a];
-            const double m = X[(2 * NT + t) * NS + s];
-            const double ref[4] = {m * Pz, X[(0 * NT + t) * NS + s] * Pz, X[(1 * NT + t) * NS + s] * Pz, m * D};
-            for (int k = 0; k < 4; ++k) {
-              worst = std::max(worst, std::fabs(PHI(q, k, dof) - ref[k]));
-              scale = std::max(scale, std::fabs(ref[k]));
-            }
-          }
-    if (worst > 1e-13 * std::max(1.0, scale)) return false;
-    xfrag.assign(C::XFRAG, 0.0);
-    for (int mt = 0; mt < C::MT; ++mt)
-      for (int ks = 0; ks < C::KSTEPS; ++ks)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int t = mt * 8 + lane / 4, kx = ks * 4 + lane % 4;
-          const int s = kx / 3, x = kx % 3;
-          double v = 0.0;
-          if (t < NT && s < NS) v = X[(x * NT + t) * NS + s];
-          xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
-        }
-    xplain.assign(C::XPLAIN, 0.0);
-    for (int s = 0; s < NS; ++s)
-      for (int t = 0; t < NT; ++t)
-        for (int x = 0; x < 3; ++x) xplain[(static_cast<size_t>(s) * 3 + x) * C::NTPS + t] = X[(x * NT + t) * NS + s];
-    return true;
-  }
-};
-
-template <template <int> class F, typename... Args>
-bool dispatch_p(int p, Args&&... args) {
-  switch (p) {
-    case 2: F<2>::run(args...); return true;
-    case 3: F<3>::run(args...); return true;
-    case 4: F<4>::run(args...); return true;
-    case 5: F<5>::run(args...); return true;
-    case 6: F<6>::run(args...); return true;
-    case 7: F<7>::run(args...); return true;
-    default: return false;
-  }
-}
-
-template <int P>
-struct LaunchOp {
-  static void run(const LaunchArgs& a, const SumFactTables& t, bool general, bool symmetric, cudaStream_t s) {
-    SumFactHost<P>::launch(a, t, general, symmetric, s);
-  }
-};
-template <int P>
-struct AttrOp {
-  static void run() { SumFactHost<P>::set_attrs(); }
-};
-template <int P>
-struct BuildOp {
-  static void run(pi_context* ctx, std::vector<double>& x, std::vector<double>& xp, std::vector<double>& y,
-                  std::vector<double>& t, bool& ok) {
-    ok = SumFactHost<P>::build(ctx, x, xp, y, t);
-  }
-};
-
 template <typename T>
 pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
   cudaError_t e = cudaMalloc(dst, std::max<size_t>(sizeof(T), src.size() * sizeof(T)));
@@ -213,38 +72,9 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
 
 int resolve_variant(const pi_context* ctx) {
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
-  if (ctx->p <= 2) return PI_VARIANT_DENSE;
+  if (ctx->n_eq == 1 && ctx->p <= 2) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
-
-// Fraction of the (t, t') pairs whose MMA tiles the symmetric path computes
-// (kernels_sumfact.cuh: t'-major skips t'-blocks below the t-block; natural
-// order skips n-tiles whose largest t' lies below the m-tile).
-template <int P>
-struct SymFracOp {
-  static void run(double& f) {
-    using C = SumFactConfig<P>;
-    if (C::NAG != 1) {
-      f = 1.0;
-      return;
-    }
-    long done = 0;
-    for (int t = 0; t < C::NT; ++t)
-      for (int tp = 0; tp < C::NT; ++tp) {
-        const int mt = t / 8;
-        bool comp;
-        if (C::TMAJOR) {
-          comp = tp / 8 >= mt;
-        } else {
-          // natural: columns j = tp*NV + b; count per (t, t') through b = 0
-          const int nt = (tp * C::NV) / 8;
-          comp = std::min(C::NT - 1, (nt * 8 + 7) / C::NV) >= 8 * mt;
-        }
-        done += comp;
-      }
-    f = static_cast<double>(done) / (C::NT * C::NT);
-  }
-};
 
 }  // namespace
 
@@ -266,8 +96,8 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   *out = nullptr;
   if (p < 1 || p > kMaxP)
     return set_error(err, PI_E_DOMAIN, "approximation order p=%d outside supported range [1, 7]", p);
-  if (n_eq != 1)
-    return set_error(err, PI_E_CONFIG, "n_eq=%d: this build integrates scalar weak forms (n_eq = 1)", n_eq);
+  if (n_eq != 1 && n_eq != 3)
+    return set_error(err, PI_E_CONFIG, "n_eq=%d: supported systems are n_eq = 1 (scalar) and 3 (elasticity)", n_eq);
   const int nsh = shape_count(p), nq = quad_count(p);
   if ((points || weights || shape_table) && !(points && weights && shape_table))
     return set_error(err, PI_E_CONTRACT, "pi_context_create: pass all of points/weights/shape_table or none");
@@ -324,23 +154,22 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                                 "shape table entry (q=%d, d=%d, dof=%d) is not the reference basis' structural zero",
                                 q, k, dof));
       }
-  if (p >= 2) {
-    std::vector<double> xf, xp, yl, tr;
-    bool ok = false;
-    dispatch_p<BuildOp>(p, ctx, xf, xp, yl, tr, ok);
+  if (sumfact_supported(p, n_eq)) {
+    SumFactHostTables tb;
+    const bool ok = sumfact_build(p, n_eq, ctx->h_pts.data(), ctx->h_phi.data(), nq, nsh, tb);
     ctx->tensor_ok = ok;
     if (ok) {
-      if ((st = upload(&ctx->d_xfrag, xf, err)) != PI_OK) return fail(st);
-      if ((st = upload(&ctx->d_xplain, xp, err)) != PI_OK) return fail(st);
-      if ((st = upload(&ctx->d_yline, yl, err)) != PI_OK) return fail(st);
-      if ((st = upload(&ctx->d_tri, tr, err)) != PI_OK) return fail(st);
-      dispatch_p<AttrOp>(p);
+      if ((st = upload(&ctx->d_xfrag, tb.xfrag, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_xplain, tb.xplain, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_yline, tb.yline, err)) != PI_OK) return fail(st);
+      if ((st = upload(&ctx->d_tri, tb.tri, err)) != PI_OK) return fail(st);
+      sumfact_set_attrs(p, n_eq);
     } else {
       return fail(set_error(err, PI_E_CONFIG,
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
-  if (p == 2) {
+  if (p == 2 && n_eq == 1) {
     std::vector<double> p4(4 * nq);
     for (int q = 0; q < nq; ++q) {
       p4[4 * q] = ctx->h_pts[3 * q];
@@ -400,8 +229,8 @@ pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* er
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
-  if (variant == PI_VARIANT_DENSE && ctx->p > 2)
-    return set_error(err, PI_E_CONFIG, "dense variant is built for p <= 2 only in this release");
+  if (variant == PI_VARIANT_DENSE && (ctx->p > 2 || ctx->n_eq != 1))
+    return set_error(err, PI_E_CONFIG, "dense variant is built for scalar forms at p <= 2 only in this release");
   ctx->variant = variant;
   return PI_OK;
 }
@@ -435,16 +264,24 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   a.out_layout = out_layout;
   a.ld_out = ld_out;
   a.bad = ctx->d_bad;
+  const int ne = ctx->n_eq, ncoef = 16 * ne * ne;
   bool general = false, symmetric = true;
+  int form = kFormLaplace;
   switch (coeff_mode) {
     case PI_COEFF_LAPLACE:
+      if (ne != 1) return set_error(err, PI_E_CONFIG, "Laplace coefficients need n_eq = 1 (context has %d)", ne);
       break;
     case PI_COEFF_UNIFORM:
       if (!coeff) return set_error(err, PI_E_CONTRACT, "uniform coefficient tensor is NULL");
-      std::memcpy(a.cu, coeff, sizeof(a.cu));
+      std::memcpy(a.cu, coeff, sizeof(double) * ncoef);
       general = true;
-      for (int k = 0; k < 4; ++k)
-        for (int l = 0; l < 4; ++l) symmetric = symmetric && a.cu[k * 4 + l] == a.cu[l * 4 + k];
+      form = kFormGeneral;
+      // major symmetry c[ie][je][k][l] == c[je][ie][l][k] makes K symmetric
+      for (int ie = 0; ie < ne; ++ie)
+        for (int je = 0; je < ne; ++je)
+          for (int k = 0; k < 4; ++k)
+            for (int l = 0; l < 4; ++l)
+              symmetric = symmetric && a.cu[((ie * ne + je) * 4 + k) * 4 + l] == a.cu[((je * ne + ie) * 4 + l) * 4 + k];
       break;
     case PI_COEFF_PER_ELEMENT:
       if (!coeff || coeff_ld < n_elem) return set_error(err, PI_E_CONTRACT, "per-element coefficients: bad buffer/ld");
@@ -452,6 +289,23 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
       a.coeff_ld = coeff_ld;
       general = true;
       symmetric = false;
+      form = kFormGeneral;
+      break;
+    case PI_COEFF_ELASTICITY:
+    case PI_COEFF_ELASTICITY_UNIFORM:
+      if (ne != 3) return set_error(err, PI_E_CONFIG, "elasticity needs n_eq = 3 (context has %d)", ne);
+      if (!coeff) return set_error(err, PI_E_CONTRACT, "elasticity material buffer is NULL");
+      if (coeff_mode == PI_COEFF_ELASTICITY) {
+        if (coeff_ld < n_elem) return set_error(err, PI_E_CONTRACT, "per-element material: coeff_ld < n_elem");
+        a.coeff = coeff;
+        a.coeff_ld = coeff_ld;
+      } else {
+        if (coeff[1] == 0.5)  // lame_parameters, coefficients.cpp:24-27
+          return set_error(err, PI_E_DOMAIN, "material: nu = 0.5 (incompressible) has no finite Lame lambda");
+        a.cu[0] = coeff[0];
+        a.cu[1] = coeff[1];
+      }
+      form = kFormElasticity;
       break;
     default:
       return set_error(err, PI_E_CONFIG, "unknown coefficient mode %d", coeff_mode);
@@ -459,7 +313,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int v = resolve_variant(ctx);
-  if (ctx->p == 2 && v == PI_VARIANT_DENSE) {
+  if (ctx->p == 2 && ne == 1 && v == PI_VARIANT_DENSE) {
     PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2, ctx->d_phi, sizeof(double) * kP2NQ * 4 * kP2NSH, 0,
                                     cudaMemcpyDeviceToDevice, s),
             "upload p=2 shape table");
@@ -483,7 +337,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
       p1_thread_kernel<false><<<grid, kP1Threads, 0, s>>>(a, t);
   } else {
     SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
-    dispatch_p<LaunchOp>(ctx->p, a, t, general, symmetric, s);
+    sumfact_launch(ctx->p, ne, form, symmetric, a, t, s);
   }
   PI_CUDA(cudaGetLastError(), "kernel launch");
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
@@ -571,8 +425,11 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
   if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
   if (!geom_aos || !out) return set_error(err, PI_E_CONTRACT, "NULL host buffers");
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  const int64_t kk = static_cast<int64_t>(ctx->n_shape) * ctx->n_shape;
-  const int cw = coeff_mode == PI_COEFF_PER_ELEMENT ? 16 : 0;
+  const int64_t dim = static_cast<int64_t>(ctx->n_shape) * ctx->n_eq;
+  const int64_t kk = dim * dim;
+  // per-element coefficient width: the tensor, or (E, nu) for elasticity
+  const int cw = coeff_mode == PI_COEFF_PER_ELEMENT ? 16 * ctx->n_eq * ctx->n_eq
+                                                    : coeff_mode == PI_COEFF_ELASTICITY ? 2 : 0;
   const size_t per_elem = sizeof(double) * (kk + 2 * 18 + 2 * cw);
   if (chunk_elems <= 0) {
     size_t free_b = 0, total_b = 0;
@@ -607,9 +464,9 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
     const double* cptr = coeff;
     int64_t cld = 0;
     if (cw) {
-      PI_CUDA(cudaMemcpyAsync(d_caos, coeff + 16 * done, sizeof(double) * 16 * cnt, cudaMemcpyHostToDevice, s),
+      PI_CUDA(cudaMemcpyAsync(d_caos, coeff + cw * done, sizeof(double) * cw * cnt, cudaMemcpyHostToDevice, s),
               "H2D coefficients");
-      aos_to_soa_kernel<<<static_cast<unsigned>((16 * cnt + 255) / 256), 256, 0, s>>>(d_caos, d_coef, cnt, 16, cnt);
+      aos_to_soa_kernel<<<static_cast<unsigned>((cw * cnt + 255) / 256), 256, 0, s>>>(d_caos, d_coef, cnt, cw, cnt);
       cptr = d_coef;
       cld = cnt;
     }
@@ -652,15 +509,21 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
 }
 
 double pi_flops_dense_per_element(int p, int n_eq, int coeff_mode) {
-  (void)n_eq;
   const double nsh = shape_count(p), nq = quad_count(p);
-  const double r = coeff_mode == PI_COEFF_LAPLACE ? 3.0 : 4.0;
-  return nq * (2.0 * r * nsh * nsh + (2.0 * r * r + 15.0) * nsh + 151.0);
+  if (coeff_mode == PI_COEFF_ELASTICITY || coeff_mode == PI_COEFF_ELASTICITY_UNIFORM)
+    // the reference's own elasticity model: 63-flop 3x3 block per shape pair,
+    // psi 15/shape, Jacobian 150 + dw 1 + 3 scaled moduli (flop_costs.hpp:15-41)
+    return nq * (63.0 * nsh * nsh + 15.0 * nsh + 154.0);
+  const double r = coeff_mode == PI_COEFF_LAPLACE ? 3.0 : 4.0, ne2 = static_cast<double>(n_eq) * n_eq;
+  return nq * (ne2 * (2.0 * r * nsh * nsh + 2.0 * r * r * nsh) + 15.0 * nsh + 151.0);
 }
 
 double pi_bytes_per_element(int p, int n_eq, int coeff_mode) {
   const double dim = static_cast<double>(n_eq) * shape_count(p);
-  return 8.0 * dim * dim + 144.0 + (coeff_mode == PI_COEFF_PER_ELEMENT ? 128.0 * n_eq * n_eq : 0.0);
+  const double coeff_bytes = coeff_mode == PI_COEFF_PER_ELEMENT ? 128.0 * n_eq * n_eq
+                             : coeff_mode == PI_COEFF_ELASTICITY ? 16.0
+                                                                  : 0.0;
+  return 8.0 * dim * dim + 144.0 + coeff_bytes;
 }
 
 double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
@@ -692,14 +555,20 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
     }
     return nq * (per_point + 2.0 * fma_count);
   }
-  const double nv = p + 1, nt = (p + 1) * (p + 2) / 2.0, ns = tri_point_count(p), nz = p + 1;
-  const double h_terms = general ? 16.0 / 9.0 : 1.0;
-  const double h = ns * nv * nv * 9.0 * nz * 3.0 * h_terms;
-  const double g = ns * 3.0 * nv * nsh * 3.0 * 2.0;
-  double frac = 1.0;
-  if (!general) dispatch_p<SymFracOp>(p, frac);
-  const double k = nt * 3.0 * ns * nsh * nv * 2.0 * frac;
-  return nq * per_point + h + g + k;
+  // Sum factorisation (kernels_sumfact.cuh): H over (s, a', b', x, y, z),
+  // the B-fragment values G (3 FMA each) and the DMMA GEMM (useful, i.e.
+  // unpadded, sizes; symmetric paths skip sub-diagonal tile pairs).
+  const double ne = ctx->n_eq, nv = p + 1, nve = ne * nv, nt = (p + 1) * (p + 2) / 2.0;
+  const double ns = tri_point_count(p), nz = p + 1, dim = nsh * ne;
+  const bool elastic = coeff_mode == PI_COEFF_ELASTICITY || coeff_mode == PI_COEFF_ELASTICITY_UNIFORM;
+  const double per_point_ne = ne == 1 ? per_point : 2.0 * (21 + 16) + 6 + ne * ne * (elastic ? 60.0 : 200.0);
+  const double h_terms = (general && !elastic) ? 16.0 / 9.0 : 1.0;
+  const double h = ns * nve * nve * 9.0 * nz * 3.0 * h_terms;
+  const double g = ns * 3.0 * nve * dim * 3.0 * 2.0;
+  bool symmetric = coeff_mode == PI_COEFF_LAPLACE || elastic;
+  const double frac = symmetric ? sumfact_sym_fraction(p, ctx->n_eq) : 1.0;
+  const double k = nt * 3.0 * ns * dim * nve * 2.0 * frac;
+  return nq * per_point_ne + h + g + k;
 }
 
 }  // extern "C"

@@ -1,0 +1,139 @@
+// Template host side of the sum-factorised kernels: table construction,
+// launch attributes and the persistent-grid launch for one (P, NE).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels_sumfact.cuh"
+#include "sumfact_api.hpp"
+
+namespace pib {
+
+template <int P, int NE>
+struct SumFactHost {
+  using C = SumFactConfig<P, NE>;
+  template <int FORM, bool SYM>
+  static void attr() {
+    cudaFuncSetAttribute(sumfact_kernel<P, NE, FORM, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(C::SMEM_BYTES));
+  }
+  // Persistent grid: as many CTAs as fit on the device at once (queried per
+  // instantiation), each looping over (element group, a'-group, column block) items.
+  template <int FORM, bool SYM>
+  static int resident_ctas() {
+    static int c = 0;
+    if (c == 0) {
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, NE, FORM, SYM>, C::NTHREADS,
+                                                    C::SMEM_BYTES);
+      c = std::max(1, sms * std::max(1, per_sm));
+    }
+    return c;
+  }
+  template <int FORM, bool SYM>
+  static void go(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
+    const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NITEM;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<FORM, SYM>())));
+    sumfact_kernel<P, NE, FORM, SYM><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+  }
+
+  // Builds the X fragment table, Y table and rule coordinates from the
+  // caller's rule and shape table; false if the table is not the tensor
+  // product the kernel factorises.
+  static bool build(const double* pts, const double* phi, int n_q, int n_shape, SumFactHostTables& out) {
+    constexpr int NS = C::NS, NZ = C::NZ, NV = C::NV, NT = C::NT, NSH1 = NT * NV;
+    if (n_q != NS * NZ || n_shape != NSH1) return false;
+    auto PHI = [&](int q, int k, int dof) { return phi[(static_cast<size_t>(q) * 4 + k) * NSH1 + dof]; };
+    for (int z = 0; z < NZ; ++z)
+      for (int s = 0; s < NS; ++s) {
+        const int q = z * NS + s;
+        if (pts[3 * q] != pts[3 * s] || pts[3 * q + 1] != pts[3 * s + 1] || pts[3 * q + 2] != pts[3 * z * NS + 2])
+          return false;
+      }
+    out.tri.assign(2 * NS, 0.0);
+    for (int s = 0; s < NS; ++s) {
+      out.tri[s] = pts[3 * s];
+      out.tri[NS + s] = pts[3 * s + 1];
+    }
+    // Y: P_a(z) = phi_0((t=0,a), (s=0,z)), P'_a(z) = phi_3((0,a),(0,z)) since m_0 = 1.
+    auto& yl = out.yline;
+    yl.assign(2 * NV * NZ + NZ, 0.0);
+    for (int a = 0; a < NV; ++a)
+      for (int z = 0; z < NZ; ++z) {
+        yl[z * NV + a] = PHI(z * NS, 0, a);
+        yl[NV * NZ + z * NV + a] = PHI(z * NS, 3, a);
+      }
+    for (int z = 0; z < NZ; ++z) yl[2 * NV * NZ + z] = pts[3 * z * NS + 2];
+    // X_x(t,s): x=0 dm/dxi1, 1 dm/dxi2, 2 m, read at a=0 (P_0 = 1), z=0.
+    std::vector<double> X(static_cast<size_t>(3) * NT * NS);
+    for (int t = 0; t < NT; ++t)
+      for (int s = 0; s < NS; ++s) {
+        X[(0 * NT + t) * NS + s] = PHI(s, 1, t * NV);
+        X[(1 * NT + t) * NS + s] = PHI(s, 2, t * NV);
+        X[(2 * NT + t) * NS + s] = PHI(s, 0, t * NV) / PHI(s, 0, 0);
+      }
+    // Structure check: phi_k(i,q) == X(t,s) Y(a,z) to rounding.
+    double worst = 0.0, scale = 0.0;
+    for (int z = 0; z < NZ; ++z)
+      for (int s = 0; s < NS; ++s)
+        for (int t = 0; t < NT; ++t)
+          for (int a = 0; a < NV; ++a) {
+            const int q = z * NS + s, dof = t * NV + a;
+            const double Pz = yl[z * NV + a], D = yl[NV * NZ + z * NV + a];
+            const double m = X[(2 * NT + t) * NS + s];
+            const double ref[4] = {m * Pz, X[(0 * NT + t) * NS + s] * Pz, X[(1 * NT + t) * NS + s] * Pz, m * D};
+            for (int k = 0; k < 4; ++k) {
+              worst = std::max(worst, std::fabs(PHI(q, k, dof) - ref[k]));
+              scale = std::max(scale, std::fabs(ref[k]));
+            }
+          }
+    if (worst > 1e-13 * std::max(1.0, scale)) return false;
+    out.xfrag.assign(C::XFRAG, 0.0);
+    for (int mt = 0; mt < C::MT; ++mt)
+      for (int ks = 0; ks < C::KSTEPS; ++ks)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int t = mt * 8 + lane / 4, kx = ks * 4 + lane % 4;
+          const int s = kx / 3, x = kx % 3;
+          double v = 0.0;
+          if (t < NT && s < NS) v = X[(x * NT + t) * NS + s];
+          out.xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
+        }
+    out.xplain.assign(C::XPLAIN, 0.0);
+    for (int s = 0; s < NS; ++s)
+      for (int t = 0; t < NT; ++t)
+        for (int x = 0; x < 3; ++x)
+          out.xplain[(static_cast<size_t>(s) * 3 + x) * C::NTPS + t] = X[(x * NT + t) * NS + s];
+    return true;
+  }
+
+  // Fraction of the (t, t') pairs whose MMA tiles the symmetric path computes
+  // (t'-major skips t'-blocks below the t-block; natural order skips n-tiles
+  // whose largest t' lies below the m-tile).
+  static double sym_fraction() {
+    if (C::NAG != 1 || C::NCB != 1) return 1.0;
+    long done = 0;
+    for (int t = 0; t < C::NT; ++t)
+      for (int tp = 0; tp < C::NT; ++tp) {
+        const int mt = t / 8;
+        bool comp;
+        if (C::TMAJOR) {
+          comp = tp / 8 >= mt;
+        } else {
+          const int nt = (tp * C::NVE) / 8;
+          comp = std::min(C::NT - 1, (nt * 8 + 7) / C::NVE) >= 8 * mt;
+        }
+        done += comp;
+      }
+    return static_cast<double>(done) / (C::NT * C::NT);
+  }
+  static void padded(int& cols, int& rows, int& k4) {
+    cols = C::NTILE * 8;
+    rows = C::MT * 8;
+    k4 = C::KSTEPS * 4;
+  }
+};
+
+}  // namespace pib

@@ -130,7 +130,7 @@ def test_context_argument_errors():
     with pytest.raises(pb.DomainError):
         pb.Integrator(9)
     with pytest.raises(pb.ConfigError):
-        pb.Integrator(2, n_eq=3)
+        pb.Integrator(2, n_eq=2)  # systems: n_eq = 1 or 3
     pts, w = pb.prism_quadrature(2)
     tab = pb.tabulate_shapes(2)
     with pytest.raises(pb.ConfigError):  # p mismatch (integrate_ref.cpp:36-46)

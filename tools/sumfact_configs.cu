@@ -1,0 +1,16 @@
+// Prints the launch shape / shared-memory footprint of every sum-factorised
+// instantiation (developer tool: nvcc -std=c++17 --expt-relaxed-constexpr).
+#include <cstdio>
+#include "../paper_1310_1191_b200/csrc/kernels_sumfact.cuh"
+using namespace pib;
+template <int P, int NE>
+void show() {
+  using C = SumFactConfig<P, NE>;
+  std::printf("p=%d ne=%d tmajor=%d threads=%4d warps cons=%2d prod=%d smem=%7.1f KB  NTILE=%3d NBLK=%d NAG=%2d NCB=%d items/el=%3d acc=%d\n",
+              P, NE, (int)C::TMAJOR, C::NTHREADS, C::NCW, C::NPW, C::SMEM_BYTES / 1024.0, C::NTILE, C::NBLK, C::NAG,
+              C::NCB, C::NITEM, C::WA * C::MT * C::NB * 2);
+}
+int main() {
+  show<2, 1>(); show<3, 1>(); show<4, 1>(); show<5, 1>(); show<6, 1>(); show<7, 1>();
+  show<1, 3>(); show<2, 3>(); show<3, 3>(); show<4, 3>(); show<5, 3>(); show<6, 3>(); show<7, 3>();
+}
