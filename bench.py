@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", default="2,3,4")
-    ap.add_argument("--coeff", default="laplace", choices=["laplace", "cdr"])
+    ap.add_argument("--coeff", default="laplace", choices=["laplace", "cdr", "elasticity"],
+                    help="weak form: Laplace, per-element CDR tensors, or n_eq=3 elasticity with per-element (E, nu)")
+    ap.add_argument("--out-gb", type=float, default=120.0,
+                    help="device output budget; larger steps stream through a ring of chunks")
     ap.add_argument("--nz", type=int, default=NZ_PER_RANK, help="mesh layers per rank (64 -> 1M elements)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -64,7 +67,8 @@ def dist_env():
 # ----------------------------------------------------------------- CPU legs
 def cpu_reference_rates(ps, coeff_kind, budget_s, mesh_aos, coeffs_aos):
     """Reference integrate_generic (oracle/_ref, all host threads) el/s per p on a
-    bounded sample of the same mesh.  Returns (rates, sample description, cores, kind)."""
+    bounded sample of the same mesh -- integrate_optimized, the reference's
+    fastest FP64 path, for elasticity.  Returns (rates, sample description, cores, kind)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import REF_SO, Oracle, Reference, laplace_tensor  # test infrastructure (checker)
 
@@ -76,9 +80,15 @@ def cpu_reference_rates(ps, coeff_kind, budget_s, mesh_aos, coeffs_aos):
         n = 16
         while True:
             g = mesh_aos[:n]
-            c = laplace_tensor() if coeff_kind == "laplace" else coeffs_aos[:n]
+            c = laplace_tensor() if coeff_kind == "laplace" else (coeffs_aos[:n] if coeffs_aos is not None else None)
             t0 = time.perf_counter()
-            if kind == "reference":
+            if coeff_kind == "elasticity":
+                if kind == "reference":
+                    Reference().integrate_optimized_batch(p, g, coeffs_aos[:n], threads=cores)
+                else:
+                    o = Oracle()
+                    o.integrate_batch(p, g, np.stack([o.elasticity_tensor(*m) for m in coeffs_aos[:n]]), n_eq=3)
+            elif kind == "reference":
                 _, err = Reference().integrate_batch(p, g, c, threads=cores)
                 assert err is None
             else:
@@ -162,7 +172,8 @@ def run_reference_arm(args, ps, ws, rank):
     E = 2 * NX * NY * args.nz
     n_probe = min(E, 200_000)
     mesh = pb.generate_box_mesh(NX, NY, args.nz * ws, DISTORTION, SEED, first=0, count=n_probe)
-    coeffs = pb.generate_cdr_coefficients(COEFF_SEED, 0, n_probe) if args.coeff == "cdr" else None
+    coeffs = (pb.generate_cdr_coefficients(COEFF_SEED, 0, n_probe) if args.coeff == "cdr"
+              else pb.generate_materials(0, n_probe) if args.coeff == "elasticity" else None)
     budget = 6.0  # seconds of CPU work per step
     rates, desc, cores, kind = cpu_reference_rates(ps, args.coeff, budget, mesh, coeffs)
     sys.path.insert(0, str(ROOT / "tests"))
@@ -175,9 +186,12 @@ def run_reference_arm(args, ps, ws, rank):
         for p in ps:
             c = laplace_tensor() if args.coeff == "laplace" else coeffs[: n_p[p]]
             t0 = time.perf_counter()
-            _, err = ref.integrate_batch(p, mesh[: n_p[p]], c, threads=cores)
+            if args.coeff == "elasticity":
+                ref.integrate_optimized_batch(p, mesh[: n_p[p]], c, threads=cores)
+            else:
+                _, err = ref.integrate_batch(p, mesh[: n_p[p]], c, threads=cores)
+                assert err is None
             acc[p] += time.perf_counter() - t0
-            assert err is None
 
     scratch = {p: 0.0 for p in ps}
     for _ in range(args.warmup):
@@ -225,7 +239,8 @@ def main():
 
     E = 2 * NX * NY * args.nz
     first = rank * E
-    mode = pb.LAPLACE if args.coeff == "laplace" else pb.PER_ELEMENT
+    n_eq = 3 if args.coeff == "elasticity" else 1
+    mode = {"laplace": pb.LAPLACE, "cdr": pb.PER_ELEMENT, "elasticity": pb.ELASTICITY}[args.coeff]
     # Synthetic inputs for this rank's contiguous range (host-generated, not timed).
     geom_host = pb.generate_box_mesh(NX, NY, args.nz * ws, DISTORTION, SEED, first=first, count=E, soa=True)
     geom = torch.from_numpy(geom_host).to(dev)
@@ -233,21 +248,36 @@ def main():
     coeff_host = None
     if mode == pb.PER_ELEMENT:
         coeff_host = pb.generate_cdr_coefficients(COEFF_SEED, first, E, soa=True)
+    elif mode == pb.ELASTICITY:
+        coeff_host = pb.generate_materials(first, E, soa=True)
+    if coeff_host is not None:
         coeff = torch.from_numpy(coeff_host).to(dev)
-    nsh = {p: pb.shape_count(p) for p in ps}
-    max_kk = max(nsh[p] ** 2 for p in ps)
-    out = torch.empty(E * max_kk, dtype=torch.float64, device=dev)
-    ctxs = {p: pb.Integrator(p, device=local) for p in ps}
+    dim = {p: n_eq * pb.shape_count(p) for p in ps}
+    kk = {p: dim[p] ** 2 for p in ps}
+    # Output: device resident.  A step whose matrices exceed --out-gb streams
+    # through one reused chunk buffer (the ring of SURVEY 8d: K is produced
+    # and left in HBM chunk by chunk; every element is still integrated).
+    budget = int(args.out_gb * 1e9 / 8)
+    chunk = {p: min(E, max(1, budget // kk[p])) for p in ps}
+    out = torch.empty(max(chunk[p] * kk[p] for p in ps), dtype=torch.float64, device=dev)
+    ctxs = {p: pb.Integrator(p, device=local, n_eq=n_eq) for p in ps}
     # A dedicated stream: a NULL handle would mean "the context's own stream"
     # in the C ABI, so torch's legacy default stream (handle 0) is never used.
     stream = torch.cuda.Stream(dev)
     sptr = stream.cuda_stream
+    g0 = geom.data_ptr()
+    c0 = coeff.data_ptr() if coeff is not None else None
+
+    def launch(p, lo, n):
+        ctxs[p].integrate_device(n, g0 + 8 * lo, out.data_ptr(), mode, None if c0 is None else c0 + 8 * lo,
+                                 element_id_base=first + lo, geom_ld=E, coeff_ld=E, stream=sptr)
 
     def step(events=None):
         for p in ps:
             if events is not None:
                 events[p][0].record(stream)
-            ctxs[p].integrate_device(E, geom, out, mode, coeff, element_id_base=first, stream=sptr)
+            for lo in range(0, E, chunk[p]):
+                launch(p, lo, min(chunk[p], E - lo))
             if events is not None:
                 events[p][1].record(stream)
 
@@ -283,6 +313,7 @@ def main():
     clk = clocks.summary()
     ms_per_step = elapsed_ms / args.steps
     value = ws * E * len(ps) / (ms_per_step * 1e-3)
+    launches = sum((E + chunk[p] - 1) // chunk[p] for p in ps)
 
     # -------- parity spot check of the timed outputs (not timed) --------
     parity = None
@@ -292,22 +323,32 @@ def main():
 
         worst = 0.0
         n_checked = 0
-        idx = [0, E // 3, E - 1]
-        mesh_aos = geom_host[:, idx].T.reshape(len(idx), 6, 3)
         for p in ps:
-            ctxs[p].integrate_device(E, geom, out, mode, coeff, element_id_base=first, stream=sptr)
+            lo = (E - 1) - ((E - 1) % chunk[p])  # the last chunk is the one left in the buffer
+            idx = sorted({lo, lo + (E - lo) // 2, E - 1})
+            launch(p, lo, E - lo)
             torch.cuda.synchronize(dev)
-            kk = nsh[p] ** 2
-            got = np.stack([out[i * kk:(i + 1) * kk].cpu().numpy().reshape(nsh[p], nsh[p]) for i in idx])
-            c = laplace_tensor() if mode == pb.LAPLACE else coeff_host[:, idx].T.copy()
-            if REF_SO.exists():
-                ref, err = Reference().integrate_batch(p, mesh_aos, c, threads=0)
+            got = np.stack([out[(i - lo) * kk[p]:(i - lo + 1) * kk[p]].cpu().numpy().reshape(dim[p], dim[p])
+                            for i in idx])
+            mesh_aos = geom_host[:, idx].T.reshape(len(idx), 6, 3)
+            if mode == pb.ELASTICITY:
+                mats = coeff_host[:, idx].T
+                if REF_SO.exists():
+                    ref = Reference().integrate_optimized_batch(p, mesh_aos, mats)
+                else:
+                    o = Oracle()
+                    ref = o.integrate_batch(p, mesh_aos, np.stack([o.elasticity_tensor(*m) for m in mats]), n_eq=3)
             else:
-                ref = Oracle().integrate_batch(p, mesh_aos, c)
+                c = laplace_tensor() if mode == pb.LAPLACE else coeff_host[:, idx].T.copy()
+                if REF_SO.exists():
+                    ref, err = Reference().integrate_batch(p, mesh_aos, c, threads=0)
+                else:
+                    ref = Oracle().integrate_batch(p, mesh_aos, c)
             worst = max(worst, float(rel_frobenius(ref, got, axis=(1, 2)).max()))
             n_checked += len(idx)
         parity = {"max_rel_frobenius": worst, "tolerance": 1e-12, "elements_checked": n_checked,
-                  "checker": "reference integrate_generic (oracle/_ref)" if REF_SO.exists() else "oracle port"}
+                  "checker": ("reference integrate_optimized" if mode == pb.ELASTICITY else
+                              "reference integrate_generic") + " (oracle/_ref)" if REF_SO.exists() else "oracle port"}
 
     # -------- roofline (dominant kernel = largest share of the step) --------
     dmma_tf, dfma_tf = pb.measure_fp64_peak(local)
@@ -316,12 +357,12 @@ def main():
     per_p = {}
     for p in ps:
         t = per_p_ms[p] * 1e-3
-        f_dense = pb.flops_dense_per_element(p, mode)
+        f_dense = pb.flops_dense_per_element(p, mode, n_eq)
         f_exec = ctxs[p].flops_executed_per_element(mode)
-        byts = pb.bytes_per_element(p, mode)
+        byts = pb.bytes_per_element(p, mode, n_eq)
         bound_s = max(f_dense * E / (dmma_tf * 1e12), byts * E / (hbm_peak * 1e9))
         per_p[str(p)] = {
-            "elements_per_s": E / t, "ms": per_p_ms[p],
+            "elements_per_s": E / t, "ms": per_p_ms[p], "launches": (E + chunk[p] - 1) // chunk[p],
             "dense_flop_alg_per_element": f_dense, "executed_flop_per_element": f_exec,
             "bytes_per_element": byts,
             "dense_tflops": f_dense * E / t / 1e12, "executed_tflops": f_exec * E / t / 1e12,
@@ -341,20 +382,22 @@ def main():
     if tf.exists():
         try:
             per_el = json.load(open(tf)).get(f"p{dom}_{args.coeff}")
-            traffic = per_el * E if per_el is not None else None
+            traffic = per_el * chunk[dom] if per_el is not None else None
         except Exception:
             traffic = None
+    kname = ("p1_thread_kernel" if dom == 1 else "p2_lane_kernel") if (dom <= 2 and n_eq == 1) else \
+        f"sumfact_kernel<{dom}, n_eq={n_eq}> (FP64 DMMA)"
     roofline = {
-        "bound": "tensor", "kernel": f"sumfact_kernel<{dom}> (FP64 DMMA)" if dom >= 2 else "p1_thread_kernel",
+        "bound": "tensor" if not (dom <= 2 and n_eq == 1) else "fp64", "kernel": kname,
         "achieved": d["dense_tflops"], "peak": dmma_tf, "unit": "TFLOP/s", "frac": d["dense_tflops"] / dmma_tf,
         "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/traffic.json)",
-        "algorithmic_bytes": d["bytes_per_element"] * E,
-        "achieved_note": "SURVEY 8(d) dense FLOP_alg per element x elements / kernel time; the kernel "
-                         "executes the sum-factorised algorithm with fewer FLOPs, so frac can exceed 1",
+        "algorithmic_bytes": d["bytes_per_element"] * chunk[dom],
+        "achieved_note": "SURVEY 8(d) dense FLOP_alg per element x elements / kernel time; the kernels "
+                         "execute fewer FLOPs (sum factorisation, structural zeros, symmetry), so frac can exceed 1",
         "executed_tflops": d["executed_tflops"], "executed_frac": d["executed_tflops"] / dmma_tf,
         "hbm_gbs": d["hbm_gbs"], "hbm_peak_gbs": hbm_peak, "hbm_frac": d["hbm_gbs"] / hbm_peak,
         "peak_source": f"FP64 DMMA m8n8k4 peak measured in-run (DFMA {dfma_tf:.1f} TF/s); "
-                       f"HBM from MEASURED_PEAKS.json",
+                       f"HBM from MEASURED_PEAKS.json" + ("" if peaks else " (absent: B200_PROFILING fallback)"),
     }
 
     # -------- end to end through the host-buffer C-ABI call --------
@@ -362,15 +405,19 @@ def main():
     if not args.no_e2e:
         geom_aos = torch.from_numpy(np.ascontiguousarray(geom_host.T)).pin_memory()
         coeff_aos = torch.from_numpy(np.ascontiguousarray(coeff_host.T)).pin_memory() if coeff_host is not None else None
-        host_out = torch.empty(E * max_kk, dtype=torch.float64).pin_memory()
+        host_n = {p: min(E, max(1, int(64e9 / 8) // kk[p])) for p in ps}  # pinned host output <= 64 GB
+        host_out = torch.empty(max(host_n[p] * kk[p] for p in ps), dtype=torch.float64).pin_memory()
         ga = geom_aos.numpy()
         ca = coeff_aos.numpy() if coeff_aos is not None else None
 
         def e2e_step():
             for p in ps:
                 it = ctxs[p]
-                o = host_out[: E * nsh[p] ** 2].numpy().reshape(E, nsh[p], nsh[p])
-                it.integrate_host(ga, mode, ca, element_id_base=first, out=o)
+                for lo in range(0, E, host_n[p]):
+                    n = min(host_n[p], E - lo)
+                    o = host_out[: n * kk[p]].numpy().reshape(n, dim[p], dim[p])
+                    it.integrate_host(ga[lo:lo + n], mode, None if ca is None else ca[lo:lo + n],
+                                      element_id_base=first + lo, out=o)
 
         for _ in range(max(1, min(args.warmup, 2))):
             e2e_step()
@@ -384,8 +431,9 @@ def main():
             t = torch.tensor([dt], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t[0])
-        h2d = E * 18 * 8 * len(ps) + (E * 16 * 8 * len(ps) if coeff_host is not None else 0)
-        d2h = sum(E * nsh[p] ** 2 * 8 for p in ps)
+        cw = 0 if coeff_host is None else coeff_host.shape[0]
+        h2d = E * 18 * 8 * len(ps) + E * cw * 8 * len(ps)
+        d2h = sum(E * kk[p] * 8 for p in ps)
         e2e = {"value": ws * E * len(ps) * args.steps / dt, "unit": "elements/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "pi_integrate_host (pinned host AoS geometry in, pinned host canonical K out, "
@@ -399,21 +447,25 @@ def main():
         caos = np.ascontiguousarray(coeff_host[:, :n_probe].T) if coeff_host is not None else None
         rates, desc, cores, kind = cpu_reference_rates(ps, args.coeff, args.cpu_seconds, mesh_aos, caos)
         cpu = {"value": step_rate(rates, ps), "unit": "elements/s", "cores": cores, "kind": kind,
-               "sample": desc, "per_p": {str(p): rates[p] for p in ps}}
+               "sample": desc, "per_p": {str(p): rates[p] for p in ps},
+               "reference_path": "integrate_optimized" if mode == pb.ELASTICITY else "integrate_generic"}
 
     if rank == 0:
+        form = {"laplace": "Laplace c=I", "cdr": "seeded per-element CDR tensors",
+                "elasticity": "n_eq=3 isotropic elasticity, per-element (E, nu)"}[args.coeff]
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (generate_box_mesh 128x64x(64*N), distortion 0.1, seed 42; "
-                    + ("Laplace c=I" if mode == pb.LAPLACE else "seeded per-element CDR tensors") + ")",
-            "config": {"workload": f"{args.coeff} p={','.join(map(str, ps))}, {E} prisms per GPU "
-                                   "(BASELINE configs[1])",
-                       "elements_per_gpu": E, "p": ps, "coeff": args.coeff, "parallelism": f"element-range x{ws}",
-                       "l2": "inputs (151 MB geometry) and outputs (2.6-45 GB) exceed the 126 MB L2"},
+            "data": f"synthetic (generate_box_mesh 128x64x(64*N), distortion 0.1, seed 42; {form})",
+            "config": {"workload": f"{args.coeff} p={','.join(map(str, ps))}, {E} prisms per GPU"
+                                   + (" (BASELINE configs[1])" if args.coeff == "laplace" and ps == [2, 3, 4] else ""),
+                       "elements_per_gpu": E, "p": ps, "coeff": args.coeff, "n_eq": n_eq,
+                       "parallelism": f"element-range x{ws}",
+                       "chunk_elements": {str(p): chunk[p] for p in ps},
+                       "l2": "inputs (151 MB geometry) and outputs (GBs) exceed the 126 MB L2"},
             "per_p": per_p, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * len(ps), "clocks": clk, "parity": parity,
+            "gpu_launches": args.steps * launches, "clocks": clk, "parity": parity,
         }
         print(json.dumps(line), flush=True)
     for c in ctxs.values():

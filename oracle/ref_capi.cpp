@@ -255,6 +255,49 @@ int ref_integrate_optimized(int p, const double* geom, double young, double nu, 
   }
 }
 
+// integrate_optimized over a batch with per-element materials [n][2] = (E, nu),
+// element-parallel on n_threads (<= 0: hardware_concurrency) -- the
+// reference's fastest FP64 elasticity path, used as the CPU baseline.
+int ref_integrate_optimized_batch(int p, int64_t n, const double* geom, const double* mats, double* out,
+                                  int n_threads, ref_error* err) {
+  try {
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    const int dim = 3 * shape_count(p);
+    const std::size_t kk = static_cast<std::size_t>(dim) * dim;
+    if (n_threads <= 0) n_threads = std::max(1u, std::thread::hardware_concurrency());
+    n_threads = static_cast<int>(std::min<int64_t>(n_threads, std::max<int64_t>(n, 1)));
+    std::atomic<int64_t> next{0};
+    std::atomic<int> failed{0};
+    ref_error first_err{};
+    std::mutex mu;
+    auto worker = [&]() {
+      for (;;) {
+        const int64_t e = next.fetch_add(1);
+        if (e >= n) break;
+        try {
+          const ElementStiffness a =
+              integrate_optimized(geom_from(geom + e * 18), {mats[2 * e], mats[2 * e + 1]}, shapes, rule, e);
+          std::copy(a.data.begin(), a.data.end(), out + e * kk);
+        } catch (const Error& ex) {
+          std::lock_guard<std::mutex> lock(mu);
+          if (!failed.exchange(1)) fail(&first_err, ex);
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < n_threads; ++t) pool.emplace_back(worker);
+    for (auto& t : pool) t.join();
+    if (failed) {
+      if (err) *err = first_err;
+      return first_err.code;
+    }
+    return 0;
+  } catch (const Error& e) {
+    return fail(err, e);
+  }
+}
+
 // elasticity_tensor (coefficients.cpp:40-59): [3*3*16] entries.
 int ref_elasticity_tensor(double young, double nu, double* out, ref_error* err) {
   try {

@@ -30,7 +30,7 @@ __all__ = [
     "LAPLACE", "UNIFORM", "PER_ELEMENT", "ELASTICITY", "ELASTICITY_UNIFORM", "OUT_CANONICAL", "OUT_SOA",
     "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
-    "generate_box_mesh", "generate_cdr_coefficients", "laplace_tensor",
+    "generate_box_mesh", "generate_cdr_coefficients", "generate_materials", "laplace_tensor",
     "Integrator", "run_batch", "measure_fp64_peak", "flops_dense_per_element", "bytes_per_element", "library",
 ]
 
@@ -172,6 +172,8 @@ def _addr(x):
     """Raw address of a numpy array or torch tensor (device or host)."""
     if x is None:
         return None
+    if isinstance(x, int):
+        return x
     if isinstance(x, np.ndarray):
         assert x.flags.c_contiguous
         return x.ctypes.data
@@ -241,6 +243,17 @@ def generate_cdr_coefficients(seed, first, count, soa=False, ld=None):
     _raise(library().pi_generate_cdr_coefficients(seed, first, count, int(soa), ld or 0, _ptr(out),
                                                   C.byref(err)), err)
     return out
+
+
+def generate_materials(first, count, soa=False):
+    """Synthetic per-element isotropic materials (young_E, poisson_nu), a pure
+    function of the global element id (any sub-range reproduces the full run):
+    E in [1, 2), nu in [0.2, 0.35).  AoS [count][2] or SoA [2][count]."""
+    g = np.arange(first, first + count, dtype=np.uint64)
+    u = ((g * np.uint64(2654435761)) % np.uint64(1000003)).astype(np.float64) / 1000003.0
+    v = ((g * np.uint64(40503) + np.uint64(17)) % np.uint64(999983)).astype(np.float64) / 999983.0
+    m = np.stack([1.0 + u, 0.2 + 0.15 * v])
+    return np.ascontiguousarray(m) if soa else np.ascontiguousarray(m.T)
 
 
 def laplace_tensor():
@@ -340,10 +353,8 @@ class Integrator:
             geom_ld = geom.shape[1] if hasattr(geom, "shape") else n_elem
         if coeff_ld is None and coeff_mode in (PER_ELEMENT, ELASTICITY):
             coeff_ld = coeff.shape[1] if hasattr(coeff, "shape") else n_elem
-        st = library().pi_integrate(self._h, n_elem, element_id_base, _addr(geom) if not isinstance(geom, int) else geom,
-                                    geom_ld, coeff_mode, caddr, coeff_ld or 0,
-                                    _addr(out) if not isinstance(out, int) else out, out_layout, ld_out,
-                                    stream, C.byref(err))
+        st = library().pi_integrate(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode, caddr,
+                                    coeff_ld or 0, _addr(out), out_layout, ld_out, stream, C.byref(err))
         _raise(st, err)
 
     def load_vectors_device(self, n_elem, geom, out, f=None, f_const=1.0, element_id_base=0, geom_ld=None,

@@ -156,6 +156,8 @@ class Reference:
         L.ref_gauss_legendre.argtypes = [C.c_int, _dp, _dp, C.POINTER(RefError)]
         L.ref_triangle_rule.argtypes = [C.c_int, _dp, _dp, C.POINTER(RefError)]
         L.ref_elasticity_tensor.argtypes = [C.c_double, C.c_double, _dp, C.POINTER(RefError)]
+        L.ref_integrate_optimized_batch.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp, C.c_int,
+                                                    C.POINTER(RefError)]
 
     def _check(self, rc, err):
         if rc != 0:
@@ -199,6 +201,17 @@ class Reference:
         out = np.zeros((dim, dim))
         err = RefError()
         self._check(self.lib.ref_integrate_optimized(p, _ptr(geom), young, nu, _ptr(out), C.byref(err)), err)
+        return out
+
+    def integrate_optimized_batch(self, p, geoms, mats, threads=0):
+        """integrate_optimized per element, mats [n][2] = (E, nu); element-parallel."""
+        geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
+        mats = np.ascontiguousarray(mats, dtype=np.float64).reshape(-1, 2)
+        dim = 3 * shape_count(p)
+        out = np.zeros((len(geoms), dim, dim))
+        err = RefError()
+        self._check(self.lib.ref_integrate_optimized_batch(p, len(geoms), _ptr(geoms), _ptr(mats), _ptr(out),
+                                                           threads, C.byref(err)), err)
         return out
 
 
