@@ -67,61 +67,75 @@ struct SumFactShape {
 // warp owns WA rows a' x NB n-tiles x all MT m-tiles (WA*NB*MT fragments);
 // NPW producer warps; NCB column blocks (CTAs) per (element, a'-group).
 // TMAJOR warps own NG t'-groups x NBB b values (NB = NG*NBB).
+template <bool TMAJOR_, int EPC_, int AG_, int WA_, int NG_, int NBB_, int NB_, int NPW_, int BSPLIT_, int MINB_,
+          int NCB_>
+struct SumFactLaunchP {
+  static constexpr bool TMAJOR = TMAJOR_;
+  static constexpr int EPC = EPC_, AG = AG_, WA = WA_, NG = NG_, NBB = NBB_, NB = NB_, NPW = NPW_, BSPLIT = BSPLIT_,
+                       MINB = MINB_, NCB = NCB_;
+};
 template <int P, int NE>
 struct SumFactLaunch;
-template <> struct SumFactLaunch<2, 1> {
-  static constexpr bool TMAJOR = true;
-  static constexpr int EPC = 8, AG = 3, WA = 3, NG = 1, NBB = 3, NB = 3, NPW = 4, BSPLIT = 1, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<3, 1> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 2, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 1, MINB = 2, NCB = 1;
-};
-template <> struct SumFactLaunch<4, 1> {
-  static constexpr bool TMAJOR = true;
-  static constexpr int EPC = 1, AG = 5, WA = 1, NG = 2, NBB = 5, NB = 10, NPW = 3, BSPLIT = 1, MINB = 2, NCB = 1;
-};
-template <> struct SumFactLaunch<5, 1> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 2, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<6, 1> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 4, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<7, 1> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 4, MINB = 1, NCB = 1;
-};
-// n_eq = 3 (elasticity): K is 9x larger; p >= 6 also splits columns over CTAs.
-template <> struct SumFactLaunch<1, 3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 2, AG = 6, WA = 3, NG = 0, NBB = 0, NB = 3, NPW = 2, BSPLIT = 2, MINB = 2, NCB = 1;
-};
-template <> struct SumFactLaunch<2, 3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 9, WA = 3, NG = 0, NBB = 0, NB = 7, NPW = 2, BSPLIT = 3, MINB = 2, NCB = 1;
-};
-template <> struct SumFactLaunch<3, 3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 4, WA = 2, NG = 0, NBB = 0, NB = 5, NPW = 2, BSPLIT = 3, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<4, 3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 3, WA = 1, NG = 0, NBB = 0, NB = 10, NPW = 3, BSPLIT = 5, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<5, 3> {
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 8, NPW = 2, BSPLIT = 6, MINB = 1, NCB = 1;
-};
-template <> struct SumFactLaunch<6, 3> {  // column blocks of 42 tiles = 16 t' rows
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 6, NPW = 2, BSPLIT = 7, MINB = 1, NCB = 2;
-};
-template <> struct SumFactLaunch<7, 3> {  // column blocks of 36 tiles = 12 t' rows
-  static constexpr bool TMAJOR = false;
-  static constexpr int EPC = 1, AG = 1, WA = 1, NG = 0, NBB = 0, NB = 4, NPW = 2, BSPLIT = 8, MINB = 1, NCB = 3;
-};
+// Per (p, n_eq): TMAJOR, EPC, AG, WA, NG, NBB, NB, NPW, BSPLIT, MINB, NCB.
+// Each can be overridden at build time (A/B runs, tools/ab_build.sh): a header
+// named by -DPI_SF_OVERRIDE defining PI_SF_<p>_<n_eq>.
+#ifdef PI_SF_OVERRIDE
+#include PI_SF_OVERRIDE
+#endif
+#ifndef PI_SF_2_1
+#define PI_SF_2_1 true, 8, 3, 3, 1, 3, 3, 4, 1, 1, 1
+#endif
+template <> struct SumFactLaunch<2, 1> : SumFactLaunchP<PI_SF_2_1> {};
+#ifndef PI_SF_3_1
+#define PI_SF_3_1 false, 2, 4, 2, 0, 0, 5, 2, 1, 2, 1
+#endif
+template <> struct SumFactLaunch<3, 1> : SumFactLaunchP<PI_SF_3_1> {};
+#ifndef PI_SF_4_1
+#define PI_SF_4_1 true, 2, 5, 1, 2, 5, 10, 2, 1, 1, 1
+#endif
+template <> struct SumFactLaunch<4, 1> : SumFactLaunchP<PI_SF_4_1> {};
+#ifndef PI_SF_5_1
+#define PI_SF_5_1 false, 1, 3, 1, 0, 0, 8, 2, 2, 1, 1
+#endif
+template <> struct SumFactLaunch<5, 1> : SumFactLaunchP<PI_SF_5_1> {};
+#ifndef PI_SF_6_1
+#define PI_SF_6_1 false, 1, 1, 1, 0, 0, 5, 2, 4, 1, 1
+#endif
+template <> struct SumFactLaunch<6, 1> : SumFactLaunchP<PI_SF_6_1> {};
+#ifndef PI_SF_7_1
+#define PI_SF_7_1 false, 1, 1, 1, 0, 0, 4, 2, 4, 1, 1
+#endif
+template <> struct SumFactLaunch<7, 1> : SumFactLaunchP<PI_SF_7_1> {};
+// n_eq = 3 (elasticity): K is 9x larger; p >= 6 also splits columns over CTAs
+// (column blocks of whole t' rows: 42 tiles = 16 t' at p = 6, 36 = 12 at p = 7).
+#ifndef PI_SF_1_3
+#define PI_SF_1_3 false, 2, 6, 3, 0, 0, 3, 2, 2, 2, 1
+#endif
+template <> struct SumFactLaunch<1, 3> : SumFactLaunchP<PI_SF_1_3> {};
+#ifndef PI_SF_2_3
+#define PI_SF_2_3 false, 1, 9, 3, 0, 0, 7, 2, 3, 2, 1
+#endif
+template <> struct SumFactLaunch<2, 3> : SumFactLaunchP<PI_SF_2_3> {};
+#ifndef PI_SF_3_3
+#define PI_SF_3_3 false, 1, 4, 2, 0, 0, 5, 2, 3, 1, 1
+#endif
+template <> struct SumFactLaunch<3, 3> : SumFactLaunchP<PI_SF_3_3> {};
+#ifndef PI_SF_4_3
+#define PI_SF_4_3 false, 1, 3, 1, 0, 0, 10, 3, 5, 1, 1
+#endif
+template <> struct SumFactLaunch<4, 3> : SumFactLaunchP<PI_SF_4_3> {};
+#ifndef PI_SF_5_3
+#define PI_SF_5_3 false, 1, 1, 1, 0, 0, 8, 2, 6, 1, 1
+#endif
+template <> struct SumFactLaunch<5, 3> : SumFactLaunchP<PI_SF_5_3> {};
+#ifndef PI_SF_6_3
+#define PI_SF_6_3 false, 1, 1, 1, 0, 0, 6, 2, 7, 1, 2
+#endif
+template <> struct SumFactLaunch<6, 3> : SumFactLaunchP<PI_SF_6_3> {};
+#ifndef PI_SF_7_3
+#define PI_SF_7_3 false, 1, 1, 1, 0, 0, 4, 2, 8, 1, 3
+#endif
+template <> struct SumFactLaunch<7, 3> : SumFactLaunchP<PI_SF_7_3> {};
 
 template <int P, int NE = 1>
 struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFactLaunch<P, NE> {
@@ -159,7 +173,11 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   // H for one chunk: [EPC][AG][4 s][NVE b'][3 x][4 y (padded)]
   static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NVE * 12;
   static constexpr int NBUF = 3;  // H ring depth (producers run up to NBUF chunks ahead)
-  static constexpr int MITEMS = L::EPC * 4 * S::NZ;   // points per chunk
+  // Scalar forms build M for every point of the item up front (one wide,
+  // latency-bound pass instead of one per chunk); systems (9 blocks per
+  // point) build it per chunk of 4 triangle points.
+  static constexpr bool MALL = NE == 1;
+  static constexpr int MITEMS = L::EPC * (MALL ? S::NSP : 4) * S::NZ;  // points per M pass
   static constexpr int MPITCH = MITEMS | 1;             // M stored k-major: [NE*NE][16][MPITCH]
   static constexpr int M_PER_CHUNK = NE * NE * 16 * MPITCH;
   static constexpr int NCOEF = 16 * NE * NE;            // coefficient tensor per element
@@ -168,7 +186,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int OFF_XP = OFF_XA + S::XFRAG;
   static constexpr int OFF_H = OFF_XP + XPLAIN;
   static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
-  static constexpr int OFF_GEOM = OFF_M + M_PER_CHUNK;
+  static constexpr int OFF_GEOM = OFF_M + (MALL ? 2 : 1) * M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + (L::EPC * 21 + 1) / 2 * 2;
   static constexpr int OFF_LINE = OFF_C + L::EPC * NCOEF;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
@@ -253,11 +271,10 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
     // ======================= producer warps =======================
     const int ptid = tid - 32 * C::NCW;
     int64_t gc = 0;  // chunk counter across items: selects the H buffer
-    for (int64_t it = 0; it < my_items; ++it) {
+    // Geometry / coefficients of item `it` into shared memory.
+    auto load_item = [&](int64_t it) {
       const int64_t w = blockIdx.x + it * gridDim.x;
       const int64_t e0 = (w / C::NITEM) * EPC;
-      const int agroup = static_cast<int>((w % C::NITEM) / C::NCB);
-      const bool flagger = (w % C::NITEM) == 0;  // one item per element group reports inversions
       if (ptid < EPC) {  // edge vectors of the item's elements
         const int64_t e = e0 + ptid;
         const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;  // pad with a valid element
@@ -285,35 +302,54 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
         }
       }
       named_sync(kBarProd, C::NPT);
-      for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
-        // (1) M blocks for the chunk's points: (el, sl, z)
-        for (int i = ptid; i < EPC * 4 * NZ; i += C::NPT) {
-          const int z = i % NZ, sl = (i / NZ) % 4, el = i / (4 * NZ);
-          const int s = chunk * 4 + sl;
-          double* Mi = sM + i;
-          if (s < NS) {
-            double cf[3][3];
-            const double det = jacobian_cofactors(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
-            const double w8 = sW[z * NS + s], wd = w8 * __drcp_rn(det);
-            const int64_t e = e0 + el;
-            if (!(det > 0.0) && e < args.n_elem && flagger) flag_inverted(args.bad, args.element_id_base + e);
+    };
+    // (1) M blocks of item `it`: points (el, s, z), s in [s_first, s_first + s_count),
+    // into M buffer mb (MALL: two buffers, so item it+1 is prepared while the
+    // consumers still drain item it's chunks from the H ring).
+    auto build_m = [&](int64_t it, int mb, int s_first, int s_count) {
+      const int64_t w = blockIdx.x + it * gridDim.x;
+      const int64_t e0 = (w / C::NITEM) * EPC;
+      const bool flagger = (w % C::NITEM) == 0;  // one item per element group reports inversions
+      double* sMb = sM + mb * C::M_PER_CHUNK;
+      for (int i = ptid; i < EPC * s_count * NZ; i += C::NPT) {
+        const int z = i % NZ, sl = (i / NZ) % s_count, el = i / (s_count * NZ);
+        const int s = s_first + sl;
+        double* Mi = sMb + i;
+        if (s < NS) {
+          double cf[3][3];
+          const double det = jacobian_cofactors(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
+          const double w8 = sW[z * NS + s], wd = w8 * __drcp_rn(det);
+          const int64_t e = e0 + el;
+          if (!(det > 0.0) && e < args.n_elem && flagger) flag_inverted(args.bad, args.element_id_base + e);
 #pragma unroll
-            for (int blk = 0; blk < NE * NE; ++blk) {
-              double M[16];
-              if (FORM == kFormElasticity)
-                elasticity_block(cf, wd, sC[2 * el], sC[2 * el + 1], blk / NE, blk % NE, M);
-              else
-                block_from_cofactors<GENERAL>(cf, det, w8, wd, sC + NCOEF * el + 16 * blk, M);
+          for (int blk = 0; blk < NE * NE; ++blk) {
+            double M[16];
+            if (FORM == kFormElasticity)
+              elasticity_block(cf, wd, sC[2 * el], sC[2 * el + 1], blk / NE, blk % NE, M);
+            else
+              block_from_cofactors<GENERAL>(cf, det, w8, wd, sC + NCOEF * el + 16 * blk, M);
 #pragma unroll
-              for (int k = 0; k < 16; ++k)
-                if (GENERAL || (k >= 4 && (k & 3) != 0)) Mi[(blk * 16 + k) * C::MPITCH] = M[k];
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 16 * NE * NE; ++k) Mi[k * C::MPITCH] = 0.0;
+            for (int k = 0; k < 16; ++k)
+              if (GENERAL || (k >= 4 && (k & 3) != 0)) Mi[(blk * 16 + k) * C::MPITCH] = M[k];
           }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16 * NE * NE; ++k) Mi[k * C::MPITCH] = 0.0;
         }
-        named_sync(kBarProd, C::NPT);
+      }
+      named_sync(kBarProd, C::NPT);
+    };
+    if (C::MALL && my_items > 0) {
+      load_item(0);
+      build_m(0, 0, 0, C::NSP);
+    }
+    for (int64_t it = 0; it < my_items; ++it) {
+      const int64_t w = blockIdx.x + it * gridDim.x;
+      const int agroup = static_cast<int>((w % C::NITEM) / C::NCB);
+      const int mb = C::MALL ? static_cast<int>(it & 1) : 0;
+      if (!C::MALL) load_item(it);
+      for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
+        if (!C::MALL) build_m(it, 0, chunk * 4, 4);
         const int buf = static_cast<int>(gc % C::NBUF);
         if (gc >= C::NBUF) named_sync(kBarEmpty0 + buf, C::NTHREADS);  // consumers released this buffer
         double* Hb = sH + buf * C::H_PER_BUF;
@@ -327,7 +363,8 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           double h[C::BPER][3];
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
-          const double* Mp = sM + (el * 4 + sl) * NZ;  // M_k of point z at Mp[k*MPITCH + z]
+          // M_k of point z at Mp[k*MPITCH + z]
+          const double* Mp = sM + mb * C::M_PER_CHUNK + (C::MALL ? (el * C::NSP + chunk * 4 + sl) : (el * 4 + sl)) * NZ;
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const double* Mz = Mp + z;
@@ -365,7 +402,14 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
         }
         smem_release();
         named_arrive(kBarFull0 + buf, C::NTHREADS);
-        named_sync(kBarProd, C::NPT);  // all producers done with sM / sGeom before they are rewritten
+        // per-chunk M: all producers done with sM before the next chunk rewrites it
+        if (!C::MALL) named_sync(kBarProd, C::NPT);
+      }
+      // MALL: the next item's geometry and M go into the other buffer while the
+      // consumers work through this item's buffered chunks
+      if (C::MALL && it + 1 < my_items) {
+        load_item(it + 1);
+        build_m(it + 1, mb ^ 1, 0, C::NSP);
       }
     }
     return;
