@@ -103,7 +103,7 @@ template <> struct SumFactLaunch<5, 1> : SumFactLaunchP<PI_SF_5_1> {};
 #endif
 template <> struct SumFactLaunch<6, 1> : SumFactLaunchP<PI_SF_6_1> {};
 #ifndef PI_SF_7_1
-#define PI_SF_7_1 false, 1, 1, 1, 0, 0, 4, 2, 4, 1, 1
+#define PI_SF_7_1 false, 1, 1, 1, 0, 0, 3, 4, 4, 1, 1
 #endif
 template <> struct SumFactLaunch<7, 1> : SumFactLaunchP<PI_SF_7_1> {};
 // n_eq = 3 (elasticity): K is 9x larger; p >= 6 also splits columns over CTAs

@@ -21,11 +21,18 @@ ap.add_argument("--variant", type=int, default=0)
 a = ap.parse_args()
 E = 2 * 128 * 64 * a.nz
 geom = torch.from_numpy(pb.generate_box_mesh(128, 64, a.nz, 0.1, 42, soa=True)).cuda()
-mode = pb.LAPLACE if a.coeff == "laplace" else pb.PER_ELEMENT
-coeff = torch.from_numpy(pb.generate_cdr_coefficients(42, 0, E, soa=True)).cuda() if mode else None
-nsh = pb.shape_count(a.p)
-out = torch.empty(E * nsh * nsh, dtype=torch.float64, device="cuda")
-it = pb.Integrator(a.p, variant=a.variant)
+mode = {"laplace": pb.LAPLACE, "cdr": pb.PER_ELEMENT, "elasticity": pb.ELASTICITY}[a.coeff]
+n_eq = 3 if mode == pb.ELASTICITY else 1
+coeff = None
+if mode == pb.PER_ELEMENT:
+    coeff = torch.from_numpy(pb.generate_cdr_coefficients(42, 0, E, soa=True)).cuda()
+elif mode == pb.ELASTICITY:
+    coeff = torch.from_numpy(pb.generate_materials(0, E, soa=True)).cuda()
+nsh = n_eq * pb.shape_count(a.p)
+E_out = min(E, int(60e9 / 8) // (nsh * nsh))  # launches beyond 60 GB of K integrate the first E_out prisms
+out = torch.empty(E_out * nsh * nsh, dtype=torch.float64, device="cuda")
+E = E_out
+it = pb.Integrator(a.p, n_eq=n_eq, variant=a.variant)
 s = None  # the context's own stream
 for _ in range(a.launches):
     it.integrate_device(E, geom, out, mode, coeff, stream=s)

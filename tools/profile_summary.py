@@ -39,15 +39,38 @@ def parse_launches(path):
 
 
 def kernel_key(name):
-    """'void sumfact_kernel<4, 0, 1>' -> (4, 'laplace'); p1_thread_kernel<0> -> (1, 'laplace')."""
-    inside = name.split("<")[1].rstrip(">").replace(" ", "").split(",")
+    """Kernel name -> (p, weak form): sumfact_kernel<P, NE, FORM, SYM>,
+    p1_thread_kernel<GENERAL>, p2_lane_kernel<GENERAL, SYM>."""
+    inside = name.split("<")[1].rstrip(">").replace(" ", "").replace("(int)", "").replace("(bool)", "").split(",")
+    general = lambda v: v in ("1", "true")  # noqa: E731
     if "p1_thread" in name:
-        return 1, "laplace" if inside[0] in ("0", "false") else "cdr"
+        return 1, "cdr" if general(inside[0]) else "laplace"
     if "p2_lane" in name:
-        return 2, "laplace" if inside[0] in ("0", "false") else "uniform-sym"
-    p = int(inside[0])
-    general = inside[1] in ("1", "true")
-    return p, "cdr" if general else "laplace"
+        if not general(inside[0]):
+            return 2, "laplace"
+        return 2, "uniform-sym" if general(inside[1]) else "cdr"
+    p, ne, form = int(inside[0]), int(inside[1]), int(inside[2])
+    if ne == 3:
+        return p, "elasticity" if form == 2 else "system"
+    return p, "cdr" if form == 1 else "laplace"
+
+
+NQ = {1: 6, 2: 18, 3: 48, 4: 80, 5: 150, 6: 231, 7: 336}
+
+
+def dense_flops(p, form):
+    if form == "elasticity":  # the reference's 63-flop block model (flop_costs.hpp)
+        return NQ[p] * (63 * NSH[p] ** 2 + 15 * NSH[p] + 154)
+    return (LAPLACE if form == "laplace" else CDR)[p]
+
+
+def dims(p, form):
+    return (3 if form in ("elasticity", "system") else 1) * NSH[p]
+
+
+def launch_elements(p, form):
+    """tools/prof_run.py caps K at 60 GB per launch."""
+    return min(E_SWEEP, int(60e9 / 8) // dims(p, form) ** 2)
 
 
 def full_counters(rep):
@@ -79,10 +102,10 @@ def main():
     for (i, name), m in agg.items():
         key = kernel_key(name)
         seen.setdefault(key, []).append((name, m))
-    lines = [f"# Kernel sweep `{a.tag}` (1 B200, ncu launch list, {E_SWEEP} prisms per launch, cold/serialised)", "",
-             "Dense roofline = min(FP64 peak 37.0 TF/s / FLOP_alg, HBM 6549.8 GB/s / bytes) per SURVEY.md 8(d).", "",
-             "| p | weak form | kernel | ms | elements/s | vs dense roofline | DRAM read MB | DRAM write MB | K bytes ideal MB |",
-             "|---|---|---|---|---|---|---|---|---|"]
+    lines = [f"# Kernel sweep `{a.tag}` (1 B200, ncu launch list, up to {E_SWEEP} prisms per launch, cold/serialised)", "",
+             "Dense roofline = min(FP64 peak 37.0 TF/s / FLOP_alg, HBM 6549.8 GB/s / bytes) per SURVEY.md 8(d) (elasticity: the reference's 63-flop block model).", "",
+             "| p | weak form | kernel | elements | ms | elements/s | vs dense roofline | DRAM read MB | DRAM write MB | K bytes ideal MB |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     traffic = {}
     tf = prof / "traffic.json"
     if tf.exists():
@@ -90,13 +113,14 @@ def main():
     for (p, form), lst in sorted(seen.items()):
         name, m = lst[-1]
         t = m["gpu__time_duration.sum"] * 1e-9
-        flops = (LAPLACE if form == "laplace" else CDR)[p]
-        byts = 8 * NSH[p] ** 2 + 144 + (128 if form == "cdr" else 0)
+        flops = dense_flops(p, form)
+        n = launch_elements(p, form)
+        byts = 8 * dims(p, form) ** 2 + 144 + {"cdr": 128, "elasticity": 16}.get(form, 0)
         bound = min(FP64_PEAK / flops, HBM_PEAK / byts)
         rd, wr = m.get("dram__bytes_read.sum", 0), m.get("dram__bytes_write.sum", 0)
-        lines.append(f"| {p} | {form} | `{name.replace('void ', '')}` | {t*1e3:.3f} | {E_SWEEP/t:.3e} | "
-                     f"{E_SWEEP/t/bound:.2f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {8*NSH[p]**2*E_SWEEP/1e6:.1f} |")
-        traffic[f"p{p}_{form}"] = (rd + wr) / E_SWEEP  # DRAM bytes per element (per launch / elements)
+        lines.append(f"| {p} | {form} | `{name.replace('void ', '')}` | {n} | {t*1e3:.3f} | {n/t:.3e} | "
+                     f"{n/t/bound:.2f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {8*dims(p, form)**2*n/1e6:.1f} |")
+        traffic[f"p{p}_{form}"] = (rd + wr) / n  # DRAM bytes per element (per launch / elements)
     json.dump(traffic, open(tf, "w"), indent=1)
     if a.full:
         c = full_counters(a.full)
