@@ -6,6 +6,7 @@
 //   #include "prism_b200_prismint.hpp"
 //   auto mats = prism_b200::run_batch(p, mesh, coeffs);       // kernels.cpp:485 shape
 //   auto same = prism_b200::integrate_batch(mesh, coeffs, shapes, rule);
+//   auto el   = prism_b200::run_batch(p, mesh, MaterialData{E, nu});  // elasticity, n_eq = 3
 //
 // Semantics: integrate_generic (integrate_ref.cpp:50-91) per element, in mesh
 // order, element-constant coefficients (coefficients_at_point is the
@@ -88,20 +89,50 @@ class Context {
       throw prismint::ConfigError("prism_b200: need one coefficient tensor or one per element");
     for (const auto& c : coeffs)
       if (c.n_eq != n_eq_) throw prismint::ConfigError("prism_b200: coefficient n_eq mismatch");
-    const std::size_t n = mesh.size();
-    std::vector<double> geom(18 * n);
-    for (std::size_t e = 0; e < n; ++e)
-      for (int v = 0; v < 6; ++v)
-        for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
     const int nc = 16 * n_eq_ * n_eq_;
     std::vector<double> cbuf(coeffs.size() * nc);
     for (std::size_t k = 0; k < coeffs.size(); ++k)
       std::memcpy(&cbuf[k * nc], coeffs[k].entries.data(), sizeof(double) * nc);
     const int mode = coeffs.size() == 1 ? PI_COEFF_UNIFORM : PI_COEFF_PER_ELEMENT;
+    return run(mesh, mode, cbuf.data(), element_id_base);
+  }
+
+  /// Isotropic elasticity (n_eq = 3 context): one material for every
+  /// element, or one per element (MaterialData, coefficients.hpp:31-34; the
+  /// material input of build_kernel_inputs, kernels.hpp:47-50).  Same result
+  /// as integrate_optimized / integrate_generic(elasticity_tensor(mat)).
+  std::vector<prismint::ElementStiffness> integrate(std::span<const prismint::PrismGeometry> mesh,
+                                                    std::span<const prismint::MaterialData> mats,
+                                                    std::int64_t element_id_base = 0) {
+    if (n_eq_ != 3) throw prismint::ConfigError("prism_b200: elasticity needs an n_eq = 3 context");
+    if (mats.empty() || (mats.size() != 1 && mats.size() != mesh.size()))
+      throw prismint::ConfigError("prism_b200: need one material or one per element");
+    for (const auto& m : mats)
+      if (m.poisson_nu == 0.5)  // lame_parameters, coefficients.cpp:24-27
+        throw prismint::DomainError("material: nu = 0.5 (incompressible) has no finite Lame lambda");
+    std::vector<double> mbuf(2 * mats.size());
+    for (std::size_t k = 0; k < mats.size(); ++k) {
+      mbuf[2 * k] = mats[k].young_E;
+      mbuf[2 * k + 1] = mats[k].poisson_nu;
+    }
+    return run(mesh, mats.size() == 1 ? PI_COEFF_ELASTICITY_UNIFORM : PI_COEFF_ELASTICITY, mbuf.data(),
+               element_id_base);
+  }
+
+  pi_context* raw() { return ctx_; }
+
+ private:
+  std::vector<prismint::ElementStiffness> run(std::span<const prismint::PrismGeometry> mesh, int mode,
+                                              const double* coeff, std::int64_t element_id_base) {
+    const std::size_t n = mesh.size();
+    std::vector<double> geom(18 * n);
+    for (std::size_t e = 0; e < n; ++e)
+      for (int v = 0; v < 6; ++v)
+        for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
     const std::size_t kk = static_cast<std::size_t>(nsh_) * n_eq_ * nsh_ * n_eq_;
     std::vector<double> out(kk * n);
     pi_error_info e{};
-    check(pi_integrate_host(ctx_, static_cast<std::int64_t>(n), element_id_base, geom.data(), mode, cbuf.data(),
+    check(pi_integrate_host(ctx_, static_cast<std::int64_t>(n), element_id_base, geom.data(), mode, coeff,
                             out.data(), 0, &e),
           e);
     std::vector<prismint::ElementStiffness> res(n);
@@ -115,9 +146,6 @@ class Context {
     return res;
   }
 
-  pi_context* raw() { return ctx_; }
-
- private:
   pi_context* ctx_ = nullptr;
   int p_ = 0, n_eq_ = 1, nsh_ = 0;
 };
@@ -140,6 +168,17 @@ inline std::vector<prismint::ElementStiffness> run_batch(int p, std::span<const 
   const prismint::QuadratureRule rule = prismint::prism_quadrature(p);
   const prismint::ShapeTable shapes = prismint::tabulate_shapes(p, rule);
   return integrate_batch(mesh, std::span<const prismint::CoefficientTensor>(&coeff, 1), shapes, rule, device);
+}
+
+/// run_batch for the reference's model problem (kernels.hpp:73-75 takes one
+/// MaterialData for the mesh): FP64 isotropic elasticity, n_eq = 3, mesh order.
+inline std::vector<prismint::ElementStiffness> run_batch(int p, std::span<const prismint::PrismGeometry> mesh,
+                                                         const prismint::MaterialData& mat, int device = 0) {
+  if (mesh.empty()) throw prismint::ConfigError("run_batch: empty mesh");
+  const prismint::QuadratureRule rule = prismint::prism_quadrature(p);
+  const prismint::ShapeTable shapes = prismint::tabulate_shapes(p, rule);
+  Context ctx(shapes, rule, 3, device);
+  return ctx.integrate(mesh, std::span<const prismint::MaterialData>(&mat, 1));
 }
 
 }  // namespace prism_b200

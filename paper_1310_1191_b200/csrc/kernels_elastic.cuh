@@ -1,0 +1,208 @@
+// p = 1 isotropic elasticity (n_eq = 3, K 18x18): lane = element, in
+// physical coordinates like the reference's integrate_optimized
+// (integrate_ref.cpp:93-130, the 21-term / 63-flop block of flop_costs.hpp):
+//   K[(i,ie),(j,je)] += dw [lam g_ie(i) g_je(j) + mu g_je(i) g_ie(j)
+//                           + mu d_(ie,je) g(i).g(j)]
+// with g_d(i) = psi_(d+1)(i) = sum_k phi_(k+1)(i) inv[k][d] (geometry.cpp:85-102).
+//
+// At p = 1 the sum-factorised kernel's per-item overhead dominates (one
+// 4-point chunk, a 6-row triangle factor), so this kernel keeps K in
+// registers instead:
+//  * a CTA integrates groups of 32 elements; lane l of every warp owns
+//    element l;
+//  * warp w (of 3) owns the upper-triangle 3x3 blocks of block rows w and
+//    5-w (7 blocks, 57 accumulators);
+//  * the 6 rule points' physical gradients (18 values) and dw*lam, dw*mu are
+//    computed once per element (2 points per warp) into shared memory, the
+//    structural zeros of the basis skipped at compile time (BasisPattern);
+//  * K leaves through shared-memory staging as contiguous coalesced blocks.
+#pragma once
+
+#include "kernels_common.cuh"
+#include "kernels_dense.cuh"
+
+namespace pib {
+
+constexpr int kE1NQ = 6, kE1NSH = 6, kE1DIM = 18, kE1KK = kE1DIM * kE1DIM;
+__constant__ double c_phi_e1[kE1NQ * 4 * kE1NSH];  // tabulate_shapes order [q][k][dof]
+__constant__ double c_pts_e1[kE1NQ * 4];           // xi1, xi2, xi3, w
+
+constexpr int kE1Warps = 3;
+constexpr int kE1Pitch = kE1KK + 1;  // odd pitch: staged elements hit distinct banks
+constexpr int kE1Round = 8;          // elements staged per output round
+constexpr int kE1NG = 20;            // per point: g_d(i) (18), dw*lam, dw*mu
+struct E1Smem {
+  static constexpr int GBUF = kE1NQ * kE1NG * 32;
+  static constexpr int SBUF = kE1Round * kE1Pitch;
+  static constexpr int BUF = GBUF > SBUF ? GBUF : SBUF;
+  static constexpr int OFF_D = BUF;             // edge vectors [21][32]
+  static constexpr int OFF_MAT = OFF_D + 21 * 32;  // lam, mu [2][32]
+  static constexpr int DOUBLES = OFF_MAT + 2 * 32;
+  static constexpr size_t BYTES = DOUBLES * sizeof(double);
+};
+
+// block rows of warp W: W and 5-W; blocks (bi, bj >= bi); diagonal blocks keep
+// the 6 entries ie <= je.
+template <int W>
+__device__ __forceinline__ constexpr int e1_brow(int r) {
+  return r == 0 ? W : kE1NSH - 1 - W;
+}
+
+template <int W>
+__device__ __forceinline__ void e1_accumulate(const double* __restrict__ sG, int lane, double* acc) {
+#pragma unroll 1
+  for (int q = 0; q < kE1NQ; ++q) {
+    const double* gq = sG + q * kE1NG * 32 + lane;
+    double g[kE1NSH][3];
+#pragma unroll
+    for (int i = 0; i < kE1NSH; ++i)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) g[i][d] = gq[(i * 3 + d) * 32];
+    const double lam = gq[18 * 32], mu = gq[19 * 32];
+    int off = 0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int bi = e1_brow<W>(r);
+      double lg[3], mg[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        lg[d] = lam * g[bi][d];
+        mg[d] = mu * g[bi][d];
+      }
+#pragma unroll
+      for (int bj = bi; bj < kE1NSH; ++bj) {
+        const double dot = mu * fma(g[bi][0], g[bj][0], fma(g[bi][1], g[bj][1], g[bi][2] * g[bj][2]));
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+          for (int je = (bj == bi ? ie : 0); je < 3; ++je) {
+            double v = fma(lg[ie], g[bj][je], fma(mg[je], g[bj][ie], acc[off]));
+            if (ie == je) v += dot;
+            acc[off++] = v;
+          }
+      }
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void e1_store(double* st, int64_t ld, bool soa, const double* acc) {
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int bi = e1_brow<W>(r);
+#pragma unroll
+    for (int bj = bi; bj < kE1NSH; ++bj)
+#pragma unroll
+      for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+        for (int je = (bj == bi ? ie : 0); je < 3; ++je) {
+          const int row = bi * 3 + ie, col = bj * 3 + je;
+          const double v = acc[off++];
+          st[(row * kE1DIM + col) * ld] = v;
+          if (row != col) st[(col * kE1DIM + row) * ld] = v;
+        }
+  }
+}
+
+#define E1_WARP_SWITCH(CALL) \
+  switch (warp) {            \
+    case 0: CALL(0); break;  \
+    case 1: CALL(1); break;  \
+    default: CALL(2); break; \
+  }
+
+__global__ void __launch_bounds__(32 * kE1Warps, 4) p1_elastic_lane_kernel(LaunchArgs args) {
+  using BP = BasisPattern<1>;
+  constexpr int NACC = 57;
+  extern __shared__ __align__(16) double e1_smem[];
+  double* sG = e1_smem;  // per-point data, then the output staging
+  double* sD = e1_smem + E1Smem::OFF_D;
+  double* sMat = e1_smem + E1Smem::OFF_MAT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t groups = (args.n_elem + 31) / 32;
+  for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
+    const int64_t e = grp * 32 + lane;
+    const bool live = e < args.n_elem;
+    const int64_t ec = live ? e : args.n_elem - 1;
+    if (warp == 0) {
+      double x[18], d[21];
+#pragma unroll
+      for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + ec];
+      prism_edges(x, d);
+#pragma unroll
+      for (int c = 0; c < 21; ++c) sD[c * 32 + lane] = d[c];
+    } else if (warp == 1) {
+      const double young = args.coeff ? args.coeff[ec] : args.cu[0];
+      const double nu = args.coeff ? args.coeff[args.coeff_ld + ec] : args.cu[1];
+      lame(young, nu, sMat[lane], sMat[32 + lane]);
+    }
+    __syncthreads();
+    // physical gradients at the warp's points
+    {
+      bool inverted = false;
+#pragma unroll
+      for (int q = warp; q < kE1NQ; q += kE1Warps) {
+        double cf[3][3];
+        const double det = jacobian_cofactors<32>(sD + lane, c_pts_e1[4 * q], c_pts_e1[4 * q + 1],
+                                                  c_pts_e1[4 * q + 2], cf);
+        inverted |= !(det > 0.0);
+        const double id = __drcp_rn(det), dw = det * c_pts_e1[4 * q + 3];
+        const double* ph = c_phi_e1 + q * 4 * kE1NSH;
+        double* gq = sG + q * kE1NG * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < kE1NSH; ++i)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            // inv[k][d] = cf[d][k] / det
+            double s = 0.0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (BP::nz(k + 1, i)) s = fma(ph[(k + 1) * kE1NSH + i], cf[d][k], s);
+            gq[(i * 3 + d) * 32] = s * id;
+          }
+        gq[18 * 32] = dw * sMat[lane];
+        gq[19 * 32] = dw * sMat[32 + lane];
+      }
+      if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
+    }
+    __syncthreads();
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+#define E1_ACC(W) e1_accumulate<W>(sG, lane, acc)
+    E1_WARP_SWITCH(E1_ACC)
+#undef E1_ACC
+    __syncthreads();  // per-point data no longer read: the buffer becomes the output staging
+    if (args.out_layout == PI_OUT_SOA) {
+      if (live) {
+#define E1_SOA(W) e1_store<W>(args.out + e, args.ld_out, true, acc)
+        E1_WARP_SWITCH(E1_SOA)
+#undef E1_SOA
+      }
+      continue;
+    }
+#pragma unroll 1
+    for (int h = 0; h < 32 / kE1Round; ++h) {
+      if (lane / kE1Round == h) {
+        double* st = sG + (lane % kE1Round) * kE1Pitch;
+#define E1_STAGE(W) e1_store<W>(st, 1, false, acc)
+        E1_WARP_SWITCH(E1_STAGE)
+#undef E1_STAGE
+      }
+      __syncthreads();
+      const int64_t first = grp * 32 + kE1Round * h;
+      const int64_t left = args.n_elem - first;
+      const int n_here = left <= 0 ? 0 : (left < kE1Round ? static_cast<int>(left) : kE1Round);
+      double* dst = args.out + first * kE1KK;
+      for (int r = threadIdx.x; r < n_here * kE1KK; r += 32 * kE1Warps) {
+        const int el = r / kE1KK, c = r - el * kE1KK;
+        dst[r] = sG[el * kE1Pitch + c];
+      }
+      __syncthreads();
+    }
+  }
+}
+#undef E1_WARP_SWITCH
+
+}  // namespace pib

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "kernels_dense.cuh"
+#include "kernels_elastic.cuh"
 #include "kernels_p2.cuh"
 #include "kernels_sumfact.cuh"
 #include "sumfact_api.hpp"
@@ -31,6 +32,7 @@ struct pi_context {
   bool tensor_ok = false;
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
+  int e1_ctas = 0;             // persistent grid of p1_elastic_lane_kernel
   double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
@@ -72,7 +74,7 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
 
 int resolve_variant(const pi_context* ctx) {
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
-  if (ctx->n_eq == 1 && ctx->p <= 2) return PI_VARIANT_DENSE;
+  if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p == 1)) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
 
@@ -169,7 +171,15 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
-  if (p == 2 && n_eq == 1) {
+  if (p == 1 && n_eq == 3) {
+    cudaFuncSetAttribute(p1_elastic_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(E1Smem::BYTES));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p1_elastic_lane_kernel, 32 * kE1Warps, E1Smem::BYTES);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->e1_ctas = std::max(1, per_sm) * sms;
+  }
+  if (p <= 2) {
     std::vector<double> p4(4 * nq);
     for (int q = 0; q < nq; ++q) {
       p4[4 * q] = ctx->h_pts[3 * q];
@@ -178,6 +188,8 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
       p4[4 * q + 3] = ctx->h_w[q];
     }
     if ((st = upload(&ctx->d_pts4, p4, err)) != PI_OK) return fail(st);
+  }
+  if (p == 2 && n_eq == 1) {
     cudaFuncSetAttribute(p2_lane_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(P2Cfg<false, true>::SMEM_BYTES));
     cudaFuncSetAttribute(p2_lane_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -229,8 +241,8 @@ pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* er
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
-  if (variant == PI_VARIANT_DENSE && (ctx->p > 2 || ctx->n_eq != 1))
-    return set_error(err, PI_E_CONFIG, "dense variant is built for scalar forms at p <= 2 only in this release");
+  if (variant == PI_VARIANT_DENSE && !((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p == 1)))
+    return set_error(err, PI_E_CONFIG, "dense variant is built for scalar forms at p <= 2 and elasticity at p = 1");
   ctx->variant = variant;
   return PI_OK;
 }
@@ -313,7 +325,16 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int v = resolve_variant(ctx);
-  if (ctx->p == 2 && ne == 1 && v == PI_VARIANT_DENSE) {
+  const bool e1_lane = ne == 3 && ctx->p == 1 && v == PI_VARIANT_DENSE && form == kFormElasticity;
+  if (e1_lane) {
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e1, ctx->d_phi, sizeof(double) * kE1NQ * 4 * kE1NSH, 0,
+                                    cudaMemcpyDeviceToDevice, s),
+            "upload p=1 shape table");
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_e1, ctx->d_pts4, sizeof(double) * kE1NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
+            "upload p=1 rule");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + 31) / 32, ctx->e1_ctas));
+    p1_elastic_lane_kernel<<<grid, 32 * kE1Warps, E1Smem::BYTES, s>>>(a);
+  } else if (ctx->p == 2 && ne == 1 && v == PI_VARIANT_DENSE) {
     PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2, ctx->d_phi, sizeof(double) * kP2NQ * 4 * kP2NSH, 0,
                                     cudaMemcpyDeviceToDevice, s),
             "upload p=2 shape table");
@@ -328,7 +349,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
       p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
     else
       p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
-  } else if (v == PI_VARIANT_DENSE) {
+  } else if (v == PI_VARIANT_DENSE && ne == 1) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     const unsigned grid = static_cast<unsigned>((n_elem + kP1Threads - 1) / kP1Threads);
     if (general)
@@ -535,6 +556,12 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   // reciprocal ~6, M block 24 (Laplace) / ~100 (general), in FLOPs.
   const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
   const int v = resolve_variant(ctx);
+  if (v == PI_VARIANT_DENSE && ctx->n_eq == 3) {
+    // p1_elastic_lane_kernel: Jacobian/cofactors, 18 physical gradients
+    // (7 structural non-zeros x 3), then 3 warps x (57 entries x 2 FMA +
+    // 7 block dot products + 12 scaled gradients) per point
+    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 7 * 3 + 2.0 * 3 * (57 * 2 + 7 * 3 + 12));
+  }
   if (v == PI_VARIANT_DENSE) {
     // G_l(i) = sum_k phi_k(i) M_kl and K_ij += sum_l G_l(i) phi_l(j) over the
     // basis' structural non-zeros (BasisPattern); upper triangle when K is

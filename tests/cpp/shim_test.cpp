@@ -59,6 +59,25 @@ int main() {
     std::printf("per-element coefficients p=3: %.3e\n", worst);
     if (!(worst <= 1e-12)) ++failures;
   }
+  // elasticity (the reference's model problem): run_batch(MaterialData) and
+  // per-element materials vs integrate_optimized
+  for (int p : {1, 2, 4}) {
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    const MaterialData mat{2.0, 0.3};
+    const auto got = prism_b200::run_batch(p, mesh, mat);
+    std::vector<MaterialData> mats;
+    for (size_t e = 0; e < mesh.size(); ++e) mats.push_back({1.0 + 0.1 * e, 0.25 + 0.01 * (e % 7)});
+    prism_b200::Context ctx(shapes, rule, 3);
+    const auto got_pe = ctx.integrate(mesh, std::span<const MaterialData>(mats));
+    double worst = 0;
+    for (size_t e = 0; e < mesh.size(); e += (p >= 4 ? 5 : 1)) {
+      worst = std::max(worst, rel_frob(integrate_optimized(mesh[e], mat, shapes, rule).data, got[e].data));
+      worst = std::max(worst, rel_frob(integrate_optimized(mesh[e], mats[e], shapes, rule).data, got_pe[e].data));
+    }
+    std::printf("p=%d elasticity vs integrate_optimized: %.3e\n", p, worst);
+    if (!(worst <= 1e-12)) ++failures;
+  }
   // error mapping: inverted element with batch offset, table mismatch
   {
     auto bad = generate_box_mesh(2, 2, 1, 0.0);
