@@ -147,6 +147,24 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
                             const double* geom_aos, int coeff_mode, const double* coeff, double* out,
                             int64_t chunk_elems, pi_error_info* err);
 
+/* ---- stiffness containers (host I/O) ---- */
+enum {
+  PI_STIFFNESS_PRISTIF1 = 1, /* the reference's single-element f32 container: save_stiffness /
+                                load_stiffness (io.cpp:112-168), byte-compatible */
+  PI_STIFFNESS_PRISTIF2 = 2  /* FP64 batch container: magic "PRISTIF2", u32 LE header length, JSON
+                                header (count, dim, dtype "f64", element_id_base, layout, n_eq,
+                                n_shape, p), count x dim x dim LE float64 in mesh order */
+};
+/* k: host canonical [count][dim][dim]; PRISTIF1 needs count == 1 and stores
+ * element_id_base as its element_id. */
+pi_status pi_save_stiffness(const char* path, int format, int p, int n_eq, int64_t count,
+                            int64_t element_id_base, const double* k, pi_error_info* err);
+/* Header of a PRISTIF1 / PRISTIF2 file (any pointer may be NULL). */
+pi_status pi_stiffness_info(const char* path, int* format, int* p, int* n_eq, int64_t* count,
+                            int64_t* element_id_base, pi_error_info* err);
+/* Payload as doubles into out[capacity] (PRISTIF1 widened from f32). */
+pi_status pi_load_stiffness(const char* path, double* out, int64_t capacity, pi_error_info* err);
+
 /* Algorithmic work per element: the dense FLOP_alg and the
  * FLOPs the selected strategy actually executes; bytes = K written +
  * geometry read (+ coefficients). */

@@ -18,6 +18,9 @@
 #include <vector>
 
 #include "prismint/coefficients.hpp"
+#ifdef PRISM_REF_IO
+#include "prismint/io.hpp"
+#endif
 #include "prismint/errors.hpp"
 #include "prismint/geometry.hpp"
 #include "prismint/integrate_ref.hpp"
@@ -308,5 +311,35 @@ int ref_elasticity_tensor(double young, double nu, double* out, ref_error* err) 
     return fail(err, e);
   }
 }
+
+#ifdef PRISM_REF_IO
+// save_stiffness / load_stiffness (io.cpp:112-168), the PRISTIF1 container.
+int ref_save_stiffness(const char* path, int p, int n_eq, const double* k, int64_t element_id, ref_error* err) {
+  try {
+    ElementStiffness a;
+    a.order_p = p;
+    a.n_eq = n_eq;
+    a.n_shape = shape_count(p);
+    a.data.assign(k, k + static_cast<std::size_t>(a.dim()) * a.dim());
+    save_stiffness(path, a, element_id);
+    return 0;
+  } catch (const Error& e) {
+    return fail(err, e);
+  }
+}
+int ref_load_stiffness(const char* path, double* out, int64_t capacity, int64_t* element_id, int* p, int* n_eq,
+                       ref_error* err) {
+  try {
+    const ElementStiffness a = load_stiffness(path, element_id);
+    if (static_cast<int64_t>(a.data.size()) > capacity) return -1;
+    std::copy(a.data.begin(), a.data.end(), out);
+    *p = a.order_p;
+    *n_eq = a.n_eq;
+    return 0;
+  } catch (const Error& e) {
+    return fail(err, e);
+  }
+}
+#endif
 
 }  // extern "C"

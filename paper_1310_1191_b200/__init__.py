@@ -31,7 +31,8 @@ __all__ = [
     "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
     "generate_box_mesh", "generate_cdr_coefficients", "generate_materials", "laplace_tensor",
-    "Integrator", "run_batch", "measure_fp64_peak", "flops_dense_per_element", "bytes_per_element", "library",
+    "Integrator", "run_batch", "measure_fp64_peak", "PRISTIF1", "PRISTIF2", "save_stiffness", "load_stiffness",
+    "stiffness_info", "flops_dense_per_element", "bytes_per_element", "library",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -147,6 +148,10 @@ def library():
     L.pi_bytes_per_element.argtypes = [C.c_int, C.c_int, C.c_int]
     L.pi_bytes_per_element.restype = C.c_double
     L.pi_measure_fp64_peak.argtypes = [C.c_int, _dp, _dp]
+    L.pi_save_stiffness.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int64, vp, E]
+    L.pi_stiffness_info.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_int64), E]
+    L.pi_load_stiffness.argtypes = [C.c_char_p, vp, C.c_int64, E]
     L.pi_status_name.restype = C.c_char_p
     L.pi_version.restype = C.c_char_p
     _lib = L
@@ -269,6 +274,42 @@ def flops_dense_per_element(p, coeff_mode=LAPLACE, n_eq=1):
 
 def bytes_per_element(p, coeff_mode=LAPLACE, n_eq=1):
     return library().pi_bytes_per_element(p, n_eq, coeff_mode)
+
+
+PRISTIF1, PRISTIF2 = 1, 2
+
+
+def save_stiffness(path, k, p, n_eq=1, element_id_base=0, fmt=PRISTIF2):
+    """Stiffness container (SURVEY 8f f4).  PRISTIF2: FP64 batch [count][dim][dim];
+    PRISTIF1: the reference's single-element f32 container (io.cpp:112-127)."""
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    dim = n_eq * shape_count(p)
+    count = k.size // (dim * dim)
+    if count * dim * dim != k.size:
+        raise ContractViolation(f"matrix size {k.size} is not a multiple of dim^2 = {dim * dim}")
+    err = _ErrInfo()
+    _raise(library().pi_save_stiffness(str(path).encode(), fmt, p, n_eq, count, element_id_base, _addr(k),
+                                       C.byref(err)), err)
+
+
+def stiffness_info(path):
+    fmt, p, n_eq = C.c_int(), C.c_int(), C.c_int()
+    count, base = C.c_int64(), C.c_int64()
+    err = _ErrInfo()
+    _raise(library().pi_stiffness_info(str(path).encode(), C.byref(fmt), C.byref(p), C.byref(n_eq), C.byref(count),
+                                       C.byref(base), C.byref(err)), err)
+    return {"format": fmt.value, "p": p.value, "n_eq": n_eq.value, "count": count.value,
+            "element_id_base": base.value}
+
+
+def load_stiffness(path):
+    """(matrices [count][dim][dim] float64, info dict) -- io.cpp:129-168 for PRISTIF1."""
+    info = stiffness_info(path)
+    dim = info["n_eq"] * shape_count(info["p"])
+    out = np.empty((info["count"], dim, dim))
+    err = _ErrInfo()
+    _raise(library().pi_load_stiffness(str(path).encode(), _addr(out), out.size, C.byref(err)), err)
+    return out, info
 
 
 def measure_fp64_peak(device=0):

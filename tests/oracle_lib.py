@@ -158,6 +158,11 @@ class Reference:
         L.ref_elasticity_tensor.argtypes = [C.c_double, C.c_double, _dp, C.POINTER(RefError)]
         L.ref_integrate_optimized_batch.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp, C.c_int,
                                                     C.POINTER(RefError)]
+        self.has_io = hasattr(L, "ref_save_stiffness")
+        if self.has_io:
+            L.ref_save_stiffness.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_int64, C.POINTER(RefError)]
+            L.ref_load_stiffness.argtypes = [C.c_char_p, _dp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int),
+                                             C.POINTER(C.c_int), C.POINTER(RefError)]
 
     def _check(self, rc, err):
         if rc != 0:
@@ -202,6 +207,22 @@ class Reference:
         err = RefError()
         self._check(self.lib.ref_integrate_optimized(p, _ptr(geom), young, nu, _ptr(out), C.byref(err)), err)
         return out
+
+    def save_stiffness(self, path, p, n_eq, k, element_id):
+        """The reference's save_stiffness (io.cpp:112-127), PRISTIF1."""
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        err = RefError()
+        self._check(self.lib.ref_save_stiffness(str(path).encode(), p, n_eq, _ptr(k), element_id, C.byref(err)), err)
+
+    def load_stiffness(self, path, capacity=2 ** 22):
+        """The reference's load_stiffness (io.cpp:129-168): (matrix, element_id, p, n_eq)."""
+        out = np.zeros(capacity)
+        eid, p, n_eq = C.c_int64(), C.c_int(), C.c_int()
+        err = RefError()
+        self._check(self.lib.ref_load_stiffness(str(path).encode(), _ptr(out), capacity, C.byref(eid), C.byref(p),
+                                                C.byref(n_eq), C.byref(err)), err)
+        dim = n_eq.value * shape_count(p.value)
+        return out[:dim * dim].reshape(dim, dim), eid.value, p.value, n_eq.value
 
     def integrate_optimized_batch(self, p, geoms, mats, threads=0):
         """integrate_optimized per element, mats [n][2] = (E, nu); element-parallel."""
