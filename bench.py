@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--p", default="2,3,4")
     ap.add_argument("--coeff", default="laplace", choices=["laplace", "cdr", "elasticity"],
                     help="weak form: Laplace, per-element CDR tensors, or n_eq=3 elasticity with per-element (E, nu)")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="K output precision (f32: the FP32 output variant, SURVEY 8f row f3)")
     ap.add_argument("--out-gb", type=float, default=120.0,
                     help="device output budget; larger steps stream through a ring of chunks")
     ap.add_argument("--nz", type=int, default=NZ_PER_RANK, help="mesh layers per rank (64 -> 1M elements)")
@@ -257,9 +259,11 @@ def main():
     # Output: device resident.  A step whose matrices exceed --out-gb streams
     # through one reused chunk buffer (the ring of SURVEY 8d: K is produced
     # and left in HBM chunk by chunk; every element is still integrated).
-    budget = int(args.out_gb * 1e9 / 8)
+    esz = 4 if args.precision == "f32" else 8
+    budget = int(args.out_gb * 1e9 / esz)
     chunk = {p: min(E, max(1, budget // kk[p])) for p in ps}
-    out = torch.empty(max(chunk[p] * kk[p] for p in ps), dtype=torch.float64, device=dev)
+    out = torch.empty(max(chunk[p] * kk[p] for p in ps), dtype=torch.float32 if esz == 4 else torch.float64,
+                      device=dev)
     ctxs = {p: pb.Integrator(p, device=local, n_eq=n_eq) for p in ps}
     # A dedicated stream: a NULL handle would mean "the context's own stream"
     # in the C ABI, so torch's legacy default stream (handle 0) is never used.
@@ -270,7 +274,8 @@ def main():
 
     def launch(p, lo, n):
         ctxs[p].integrate_device(n, g0 + 8 * lo, out.data_ptr(), mode, None if c0 is None else c0 + 8 * lo,
-                                 element_id_base=first + lo, geom_ld=E, coeff_ld=E, stream=sptr)
+                                 element_id_base=first + lo, geom_ld=E, coeff_ld=E, stream=sptr,
+                                 precision=args.precision)
 
     def step(events=None):
         for p in ps:
@@ -328,7 +333,7 @@ def main():
             idx = sorted({lo, lo + (E - lo) // 2, E - 1})
             launch(p, lo, E - lo)
             torch.cuda.synchronize(dev)
-            got = np.stack([out[(i - lo) * kk[p]:(i - lo + 1) * kk[p]].cpu().numpy().reshape(dim[p], dim[p])
+            got = np.stack([out[(i - lo) * kk[p]:(i - lo + 1) * kk[p]].double().cpu().numpy().reshape(dim[p], dim[p])
                             for i in idx])
             mesh_aos = geom_host[:, idx].T.reshape(len(idx), 6, 3)
             if mode == pb.ELASTICITY:
@@ -346,7 +351,7 @@ def main():
                     ref = Oracle().integrate_batch(p, mesh_aos, c)
             worst = max(worst, float(rel_frobenius(ref, got, axis=(1, 2)).max()))
             n_checked += len(idx)
-        parity = {"max_rel_frobenius": worst, "tolerance": 1e-12, "elements_checked": n_checked,
+        parity = {"max_rel_frobenius": worst, "tolerance": 1e-12 if esz == 8 else 5e-5, "elements_checked": n_checked,
                   "checker": ("reference integrate_optimized" if mode == pb.ELASTICITY else
                               "reference integrate_generic") + " (oracle/_ref)" if REF_SO.exists() else "oracle port"}
 
@@ -359,7 +364,7 @@ def main():
         t = per_p_ms[p] * 1e-3
         f_dense = pb.flops_dense_per_element(p, mode, n_eq)
         f_exec = ctxs[p].flops_executed_per_element(mode)
-        byts = pb.bytes_per_element(p, mode, n_eq)
+        byts = pb.bytes_per_element(p, mode, n_eq) - (8 - esz) * kk[p]
         bound_s = max(f_dense * E / (dmma_tf * 1e12), byts * E / (hbm_peak * 1e9))
         per_p[str(p)] = {
             "elements_per_s": E / t, "ms": per_p_ms[p], "launches": (E + chunk[p] - 1) // chunk[p],
@@ -402,7 +407,7 @@ def main():
 
     # -------- end to end through the host-buffer C-ABI call --------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and esz == 8:
         geom_aos = torch.from_numpy(np.ascontiguousarray(geom_host.T)).pin_memory()
         coeff_aos = torch.from_numpy(np.ascontiguousarray(coeff_host.T)).pin_memory() if coeff_host is not None else None
         host_n = {p: min(E, max(1, int(64e9 / 8) // kk[p])) for p in ps}  # pinned host output <= 64 GB
@@ -456,11 +461,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if esz == 8 else "f64 compute, f32 K",
             "data": f"synthetic (generate_box_mesh 128x64x(64*N), distortion 0.1, seed 42; {form})",
             "config": {"workload": f"{args.coeff} p={','.join(map(str, ps))}, {E} prisms per GPU"
                                    + (" (BASELINE configs[1])" if args.coeff == "laplace" and ps == [2, 3, 4] else ""),
-                       "elements_per_gpu": E, "p": ps, "coeff": args.coeff, "n_eq": n_eq,
+                       "elements_per_gpu": E, "p": ps, "coeff": args.coeff, "n_eq": n_eq, "precision": args.precision,
                        "parallelism": f"element-range x{ws}",
                        "chunk_elements": {str(p): chunk[p] for p in ps},
                        "l2": "inputs (151 MB geometry) and outputs (GBs) exceed the 126 MB L2"},

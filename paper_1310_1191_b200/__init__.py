@@ -138,6 +138,7 @@ def library():
     L.pi_context_stream.restype = vp
     L.pi_integrate.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, C.c_int,
                                C.c_int64, vp, E]
+    L.pi_integrate_f32.argtypes = L.pi_integrate.argtypes
     L.pi_load_vectors.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_double, vp, vp, E]
     L.pi_check.argtypes = [vp, E]
     L.pi_integrate_host.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int, vp, vp, C.c_int64, E]
@@ -381,8 +382,10 @@ class Integrator:
 
     # -- device buffers (torch tensors or raw addresses); asynchronous --
     def integrate_device(self, n_elem, geom, out, coeff_mode=LAPLACE, coeff=None, element_id_base=0,
-                         geom_ld=None, coeff_ld=None, out_layout=OUT_CANONICAL, ld_out=0, stream=None):
-        """pi_integrate on device memory.  geom: SoA [18][geom_ld]; out: device buffer."""
+                         geom_ld=None, coeff_ld=None, out_layout=OUT_CANONICAL, ld_out=0, stream=None,
+                         precision=None):
+        """pi_integrate on device memory.  geom: SoA [18][geom_ld]; out: device buffer
+        (float64; float32 selects the FP32 output variant, or precision="f32" for raw addresses)."""
         err = _ErrInfo()
         cbuf = None
         if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
@@ -394,8 +397,11 @@ class Integrator:
             geom_ld = geom.shape[1] if hasattr(geom, "shape") else n_elem
         if coeff_ld is None and coeff_mode in (PER_ELEMENT, ELASTICITY):
             coeff_ld = coeff.shape[1] if hasattr(coeff, "shape") else n_elem
-        st = library().pi_integrate(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode, caddr,
-                                    coeff_ld or 0, _addr(out), out_layout, ld_out, stream, C.byref(err))
+        # float32 output buffer -> the FP32 output variant (pi_integrate_f32)
+        f32 = precision == "f32" or (precision is None and str(getattr(out, "dtype", "")) in ("torch.float32", "float32"))
+        fn = library().pi_integrate_f32 if f32 else library().pi_integrate
+        st = fn(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode, caddr, coeff_ld or 0,
+                _addr(out), out_layout, ld_out, stream, C.byref(err))
         _raise(st, err)
 
     def load_vectors_device(self, n_elem, geom, out, f=None, f_const=1.0, element_id_base=0, geom_ld=None,

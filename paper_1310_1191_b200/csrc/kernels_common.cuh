@@ -18,6 +18,7 @@ struct LaunchArgs {
   int64_t coeff_ld;
   double cu[144];       // UNIFORM coefficient tensor [n_eq][n_eq][4][4] (or E, nu)
   double* out;
+  float* out32;         // FP32 output variant (out unused): K rounded to float at the store
   int out_layout;
   int64_t ld_out;
   unsigned long long* bad;  // min offending global element id (atomicMin)
@@ -263,6 +264,26 @@ __device__ __forceinline__ void bulk_store_doubles(double* gdst, const double* s
   const int body = (n - head) & ~1;
   if (body > 0) bulk_store(gdst + head, ssrc + head, static_cast<unsigned>(body) * 8u);
   if (head + body < n) gdst[n - 1] = ssrc[n - 1];
+}
+
+// Stores one entry of K: FP64, or rounded to FP32 for the FP32 output variant.
+__device__ __forceinline__ void store_out(const LaunchArgs& a, int64_t idx, double v) {
+  if (a.out32)
+    a.out32[idx] = static_cast<float>(v);
+  else
+    a.out[idx] = v;
+}
+
+// FP32 variant of bulk_store_doubles: scalar head / tail where the global
+// address is not 16-byte aligned; src and dst agree modulo 16 bytes.
+__device__ __forceinline__ void bulk_store_floats(float* gdst, const float* ssrc, int n) {
+  int head = static_cast<int>(((16 - (reinterpret_cast<uintptr_t>(gdst) & 15)) & 15) / 4);
+  head = head < n ? head : n;
+  for (int i = 0; i < head; ++i) gdst[i] = ssrc[i];
+  const int body = (n - head) & ~3;
+  if (body > 0) bulk_store(reinterpret_cast<double*>(gdst + head), reinterpret_cast<const double*>(ssrc + head),
+                           static_cast<unsigned>(body) * 4u);
+  for (int i = head + body; i < n; ++i) gdst[i] = ssrc[i];
 }
 
 __device__ __forceinline__ void flag_inverted(unsigned long long* bad, int64_t gid) {

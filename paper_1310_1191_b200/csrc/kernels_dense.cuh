@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kP1Threads, GENERAL ? PI_P1_MINB_GENERAL : 4) 
   if (args.out_layout == PI_OUT_SOA) {
     if (live) {
 #pragma unroll
-      for (int i = 0; i < KK; ++i) args.out[i * args.ld_out + e] = K[i];
+      for (int i = 0; i < KK; ++i) store_out(args, i * args.ld_out + e, K[i]);
     }
     return;
   }
@@ -146,9 +146,14 @@ __global__ void __launch_bounds__(kP1Threads, GENERAL ? PI_P1_MINB_GENERAL : 4) 
   __syncthreads();
   const int64_t first = static_cast<int64_t>(blockIdx.x) * kP1Threads;
   const int64_t n_here = min(static_cast<int64_t>(kP1Threads), args.n_elem - first);
-  double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
   const int total2 = static_cast<int>(n_here) * (KK / 2);
-  for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
+  if (args.out32) {
+    float2* dst = reinterpret_cast<float2*>(args.out32 + first * KK);
+    for (int i = tid; i < total2; i += kP1Threads) dst[i] = make_float2(static_cast<float>(so2[i].x), static_cast<float>(so2[i].y));
+  } else {
+    double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
+    for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
+  }
 }
 
 // Load vectors: F_i = sum_q det_q w_q f phi_i(q) (value row).  One warp per

@@ -85,8 +85,8 @@ __device__ __forceinline__ void e1_accumulate(const double* __restrict__ sG, int
   }
 }
 
-template <int W>
-__device__ __forceinline__ void e1_store(double* st, int64_t ld, bool soa, const double* acc) {
+template <int W, typename T>
+__device__ __forceinline__ void e1_store(T* st, int64_t ld, const double* acc) {
   int off = 0;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -99,8 +99,8 @@ __device__ __forceinline__ void e1_store(double* st, int64_t ld, bool soa, const
         for (int je = (bj == bi ? ie : 0); je < 3; ++je) {
           const int row = bi * 3 + ie, col = bj * 3 + je;
           const double v = acc[off++];
-          st[(row * kE1DIM + col) * ld] = v;
-          if (row != col) st[(col * kE1DIM + row) * ld] = v;
+          st[(row * kE1DIM + col) * ld] = static_cast<T>(v);
+          if (row != col) st[(col * kE1DIM + row) * ld] = static_cast<T>(v);
         }
   }
 }
@@ -176,9 +176,15 @@ __global__ void __launch_bounds__(32 * kE1Warps, 4) p1_elastic_lane_kernel(Launc
     __syncthreads();  // per-point data no longer read: the buffer becomes the output staging
     if (args.out_layout == PI_OUT_SOA) {
       if (live) {
-#define E1_SOA(W) e1_store<W>(args.out + e, args.ld_out, true, acc)
-        E1_WARP_SWITCH(E1_SOA)
+        if (args.out32) {
+#define E1_SOA(W) e1_store<W>(args.out32 + e, args.ld_out, acc)
+          E1_WARP_SWITCH(E1_SOA)
 #undef E1_SOA
+        } else {
+#define E1_SOA(W) e1_store<W>(args.out + e, args.ld_out, acc)
+          E1_WARP_SWITCH(E1_SOA)
+#undef E1_SOA
+        }
       }
       continue;
     }
@@ -186,7 +192,7 @@ __global__ void __launch_bounds__(32 * kE1Warps, 4) p1_elastic_lane_kernel(Launc
     for (int h = 0; h < 32 / kE1Round; ++h) {
       if (lane / kE1Round == h) {
         double* st = sG + (lane % kE1Round) * kE1Pitch;
-#define E1_STAGE(W) e1_store<W>(st, 1, false, acc)
+#define E1_STAGE(W) e1_store<W>(st, 1, acc)
         E1_WARP_SWITCH(E1_STAGE)
 #undef E1_STAGE
       }
@@ -194,10 +200,9 @@ __global__ void __launch_bounds__(32 * kE1Warps, 4) p1_elastic_lane_kernel(Launc
       const int64_t first = grp * 32 + kE1Round * h;
       const int64_t left = args.n_elem - first;
       const int n_here = left <= 0 ? 0 : (left < kE1Round ? static_cast<int>(left) : kE1Round);
-      double* dst = args.out + first * kE1KK;
       for (int r = threadIdx.x; r < n_here * kE1KK; r += 32 * kE1Warps) {
         const int el = r / kE1KK, c = r - el * kE1KK;
-        dst[r] = sG[el * kE1Pitch + c];
+        store_out(args, first * kE1KK + r, sG[el * kE1Pitch + c]);
       }
       __syncthreads();
     }

@@ -180,8 +180,8 @@ __device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, 
 #pragma unroll
     for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
       const double v = acc[off + j - (SYM ? i : 0)];
-      args.out[(i * kP2NSH + j) * args.ld_out + e] = v;
-      if (SYM && j > i) args.out[(j * kP2NSH + i) * args.ld_out + e] = v;
+      store_out(args, (i * kP2NSH + j) * args.ld_out + e, v);
+      if (SYM && j > i) store_out(args, (j * kP2NSH + i) * args.ld_out + e, v);
     }
     off += SYM ? kP2NSH - i : kP2NSH;
   }
@@ -290,7 +290,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
 #undef P2_SOA
         } else {
 #pragma unroll
-          for (int j = 0; j < kP2NSH; ++j) args.out[(warp * kP2NSH + j) * args.ld_out + e] = acc[j];
+          for (int j = 0; j < kP2NSH; ++j) store_out(args, (warp * kP2NSH + j) * args.ld_out + e, acc[j]);
         }
       }
       continue;
@@ -312,10 +312,9 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
       const int64_t first = g * 32 + C::ROUND * h;
       const int64_t left = args.n_elem - first;
       const int n_here = left <= 0 ? 0 : (left < C::ROUND ? static_cast<int>(left) : C::ROUND);
-      double* dst = args.out + first * kP2KK;
       for (int r = threadIdx.x; r < n_here * kP2KK; r += C::NTHREADS) {
         const int el = r / kP2KK, c = r - el * kP2KK;
-        dst[r] = sM[el * kP2Pitch + c];
+        store_out(args, first * kP2KK + r, sM[el * kP2Pitch + c]);
       }
       __syncthreads();
     }

@@ -573,12 +573,24 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
     // ---- epilogue (overlaps the producers' next item) ----
     if constexpr (C::BULK) {
       // Whole element matrices in canonical order, mirrors included, then one
-      // TMA bulk store per element.
-      const bool bulk = args.out_layout == PI_OUT_CANONICAL && (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
+      // TMA bulk store per element (FP64, or rounded to FP32 in the staging
+      // buffer for the FP32 output variant).
+      const bool f32 = args.out32 != nullptr;
+      const uintptr_t obase = f32 ? reinterpret_cast<uintptr_t>(args.out32) : reinterpret_cast<uintptr_t>(args.out);
+      const bool bulk = args.out_layout == PI_OUT_CANONICAL && (obase & 15) == 0;
+      const int amask = f32 ? 3 : 1;  // staging offset so smem and global agree modulo 16 bytes
       if (tid < EPC) bulk_wait_read();  // the issuing threads: previous stores no longer read the staging buffer
       named_sync(kBarCons, 32 * C::NCW);
       const int64_t ecl = e < args.n_elem ? e : 0;
-      double* st = smem + C::OFF_STAGE + el_w * C::ESTRIDE + (bulk ? static_cast<int>((ecl * kk_elem) & 1) : 0);
+      const int soff = bulk ? static_cast<int>((ecl * kk_elem) & amask) : 0;
+      double* st = smem + C::OFF_STAGE + el_w * C::ESTRIDE + soff;
+      float* stf = reinterpret_cast<float*>(smem + C::OFF_STAGE + el_w * C::ESTRIDE) + soff;
+      auto put = [&](int idx, double v) {
+        if (f32)
+          stf[idx] = static_cast<float>(v);
+        else
+          st[idx] = v;
+      };
 #pragma unroll
       for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
@@ -594,8 +606,8 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
                 const int tp = g * 8 + 2 * (lane & 3) + h;
                 if (t < NT && tp < NT) {
                   const double v = acc[wa][mt][g * NVE + b][h];
-                  st[row * NSH + tp * NVE + b] = v;
-                  if (SYMK && g > mt) st[(tp * NVE + b) * NSH + row] = v;  // mirror of the skipped block
+                  put(row * NSH + tp * NVE + b, v);
+                  if (SYMK && g > mt) put((tp * NVE + b) * NSH + row, v);  // mirror of the skipped block
                 }
               }
         }
@@ -605,8 +617,14 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
         if (tid < EPC) {
           const int64_t ee = (w / C::NITEM) * EPC + tid;
           if (ee < args.n_elem) {
-            const double* src = smem + C::OFF_STAGE + tid * C::ESTRIDE + static_cast<int>((ee * kk_elem) & 1);
-            bulk_store_doubles(args.out + ee * kk_elem, src, static_cast<int>(kk_elem));
+            const int o = static_cast<int>((ee * kk_elem) & amask);
+            if (f32)
+              bulk_store_floats(args.out32 + ee * kk_elem,
+                                reinterpret_cast<const float*>(smem + C::OFF_STAGE + tid * C::ESTRIDE) + o,
+                                static_cast<int>(kk_elem));
+            else
+              bulk_store_doubles(args.out + ee * kk_elem, smem + C::OFF_STAGE + tid * C::ESTRIDE + o,
+                                 static_cast<int>(kk_elem));
             bulk_commit();
           }
         }
@@ -615,11 +633,13 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           const int64_t ee = (w / C::NITEM) * EPC + el;
           if (ee >= args.n_elem) break;
           const double* src = smem + C::OFF_STAGE + el * C::ESTRIDE;
+          const float* srcf = reinterpret_cast<const float*>(src);
           for (int i = tid; i < kk_elem; i += 32 * C::NCW) {
+            const double v = f32 ? static_cast<double>(srcf[i]) : src[i];
             if (args.out_layout == PI_OUT_CANONICAL)
-              args.out[ee * kk_elem + i] = src[i];
+              store_out(args, ee * kk_elem + i, v);
             else
-              args.out[i * args.ld_out + ee] = src[i];
+              store_out(args, i * args.ld_out + ee, v);
           }
         }
       }
@@ -647,19 +667,20 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
       __syncwarp();
       const int64_t row0 = agroup * AG + al0;  // row of (t = 0, wa = 0); row(t, wa) = row0 + t*NVE + wa
       if (args.out_layout == PI_OUT_CANONICAL) {
-        double* dst = args.out + e * kk_elem + row0 * NSH;
+        const int64_t dst = e * kk_elem + row0 * NSH;
 #pragma unroll
         for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
           for (int t = 0; t < NT; ++t)
 #pragma unroll
             for (int j0 = 0; j0 < NSH; j0 += 32)
-              if (j0 + lane < NSH) dst[(t * NVE + wa) * NSH + j0 + lane] = st[(wa * NT + t) * NSH + j0 + lane];
+              if (j0 + lane < NSH)
+                store_out(args, dst + (t * NVE + wa) * NSH + j0 + lane, st[(wa * NT + t) * NSH + j0 + lane]);
       } else {
         for (int r = 0; r < WA * NT; ++r) {
           const int wa = r / NT, t = r % NT;
           const int64_t row = row0 + t * NVE + wa;
-          for (int j = lane; j < NSH; j += 32) args.out[(row * NSH + j) * args.ld_out + e] = st[r * NSH + j];
+          for (int j = lane; j < NSH; j += 32) store_out(args, (row * NSH + j) * args.ld_out + e, st[r * NSH + j]);
         }
       }
       __syncwarp();
@@ -689,11 +710,11 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
                 mirror = tmax2 < 8 * mt2;
               }
               if (args.out_layout == PI_OUT_CANONICAL) {
-                args.out[e * kk_elem + static_cast<int64_t>(row) * NSH + jj] = v;
-                if (mirror) args.out[e * kk_elem + static_cast<int64_t>(jj) * NSH + row] = v;
+                store_out(args, e * kk_elem + static_cast<int64_t>(row) * NSH + jj, v);
+                if (mirror) store_out(args, e * kk_elem + static_cast<int64_t>(jj) * NSH + row, v);
               } else {
-                args.out[(static_cast<int64_t>(row) * NSH + jj) * args.ld_out + e] = v;
-                if (mirror) args.out[(static_cast<int64_t>(jj) * NSH + row) * args.ld_out + e] = v;
+                store_out(args, (static_cast<int64_t>(row) * NSH + jj) * args.ld_out + e, v);
+                if (mirror) store_out(args, (static_cast<int64_t>(jj) * NSH + row) * args.ld_out + e, v);
               }
             }
           }

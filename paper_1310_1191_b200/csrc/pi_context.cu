@@ -254,14 +254,18 @@ int pi_context_variant(const pi_context* ctx, int coeff_mode) {
 
 void* pi_context_stream(pi_context* ctx) { return ctx ? ctx->stream : nullptr; }
 
-pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
-                       int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
-                       int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
+}  // extern "C"
+
+namespace {
+// pi_integrate / pi_integrate_f32: exactly one of out, out32 is non-NULL.
+pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                         int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
+                         float* out32, int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
   if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
   if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
   if (n_elem < 0) return set_error(err, PI_E_CONTRACT, "n_elem < 0");
   if (n_elem == 0) return PI_OK;
-  if (!geom || !out) return set_error(err, PI_E_CONTRACT, "geometry/output buffers must be non-NULL");
+  if (!geom || (!out && !out32)) return set_error(err, PI_E_CONTRACT, "geometry/output buffers must be non-NULL");
   if (geom_ld < n_elem) return set_error(err, PI_E_CONTRACT, "geom_ld (%lld) < n_elem (%lld)", (long long)geom_ld,
                                          (long long)n_elem);
   if (out_layout != PI_OUT_CANONICAL && out_layout != PI_OUT_SOA)
@@ -273,6 +277,7 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   a.geom = geom;
   a.geom_ld = geom_ld;
   a.out = out;
+  a.out32 = out32;
   a.out_layout = out_layout;
   a.ld_out = ld_out;
   a.bad = ctx->d_bad;
@@ -364,6 +369,31 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
   if (ctx->calls.size() > 4096) ctx->calls.erase(ctx->calls.begin(), ctx->calls.begin() + 2048);
   return PI_OK;
+}
+}  // namespace
+
+extern "C" {
+
+pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                       int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
+                       int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
+  if (!out && n_elem > 0) {
+    if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+    return set_error(err, PI_E_CONTRACT, "geometry/output buffers must be non-NULL");
+  }
+  return integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, out, nullptr,
+                        out_layout, ld_out, stream, err);
+}
+
+pi_status pi_integrate_f32(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                           int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, float* out,
+                           int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
+  if (!out && n_elem > 0) {
+    if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+    return set_error(err, PI_E_CONTRACT, "geometry/output buffers must be non-NULL");
+  }
+  return integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, nullptr, out,
+                        out_layout, ld_out, stream, err);
 }
 
 pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
