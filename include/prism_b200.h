@@ -174,6 +174,16 @@ pi_status pi_stiffness_info(const char* path, int* format, int* p, int* n_eq, in
 /* Payload as doubles into out[capacity] (PRISTIF1 widened from f32). */
 pi_status pi_load_stiffness(const char* path, double* out, int64_t capacity, pi_error_info* err);
 
+/* Multi-GPU run_batch: the mesh is split into contiguous
+ * element ranges [floor(g*n/G), floor((g+1)*n/G)) over the G contexts (one
+ * per device; elements are independent, so there is no collective), one
+ * host thread per context, each streaming its range through
+ * pi_integrate_host.  The output is bitwise identical to a single context.
+ * Errors as a single call: the lowest inverted global element id. */
+pi_status pi_integrate_host_multi(pi_context* const* ctxs, int n_ctx, int64_t n_elem, int64_t element_id_base,
+                                  const double* geom_aos, int coeff_mode, const double* coeff, double* out,
+                                  int64_t chunk_elems, pi_error_info* err);
+
 /* Algorithmic work per element: the dense FLOP_alg and the
  * FLOPs the selected strategy actually executes; bytes = K written +
  * geometry read (+ coefficients). */

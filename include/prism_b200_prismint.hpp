@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -158,6 +159,51 @@ inline std::vector<prismint::ElementStiffness> integrate_batch(std::span<const p
                                                                std::int64_t element_id_base = 0) {
   Context ctx(shapes, rule, coeffs.empty() ? 1 : coeffs.front().n_eq, device);
   return ctx.integrate(mesh, coeffs, element_id_base);
+}
+
+/// integrate_generic for a whole mesh over several GPUs: contiguous element
+/// ranges, one context and host thread per device (pi_integrate_host_multi);
+/// bitwise equal to one device.
+inline std::vector<prismint::ElementStiffness> integrate_batch_multi(
+    std::span<const prismint::PrismGeometry> mesh, std::span<const prismint::CoefficientTensor> coeffs,
+    const prismint::ShapeTable& shapes, const prismint::QuadratureRule& rule, std::span<const int> devices,
+    std::int64_t element_id_base = 0) {
+  if (devices.empty()) throw prismint::ConfigError("prism_b200: no devices");
+  if (coeffs.empty() || (coeffs.size() != 1 && coeffs.size() != mesh.size()))
+    throw prismint::ConfigError("prism_b200: need one coefficient tensor or one per element");
+  const int n_eq = coeffs.front().n_eq;
+  std::vector<std::unique_ptr<Context>> ctx;
+  std::vector<pi_context*> raw;
+  for (int d : devices) {
+    ctx.push_back(std::make_unique<Context>(shapes, rule, n_eq, d));
+    raw.push_back(ctx.back()->raw());
+  }
+  const std::size_t n = mesh.size();
+  std::vector<double> geom(18 * n);
+  for (std::size_t e = 0; e < n; ++e)
+    for (int v = 0; v < 6; ++v)
+      for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
+  const int nc = 16 * n_eq * n_eq;
+  std::vector<double> cbuf(coeffs.size() * nc);
+  for (std::size_t k = 0; k < coeffs.size(); ++k)
+    std::memcpy(&cbuf[k * nc], coeffs[k].entries.data(), sizeof(double) * nc);
+  const int nsh = shapes.n_shape;
+  const std::size_t kk = static_cast<std::size_t>(nsh) * n_eq * nsh * n_eq;
+  std::vector<double> out(kk * n);
+  pi_error_info e{};
+  check(pi_integrate_host_multi(raw.data(), static_cast<int>(raw.size()), static_cast<std::int64_t>(n),
+                                element_id_base, geom.data(),
+                                coeffs.size() == 1 ? PI_COEFF_UNIFORM : PI_COEFF_PER_ELEMENT, cbuf.data(),
+                                out.data(), 0, &e),
+        e);
+  std::vector<prismint::ElementStiffness> res(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    res[i].order_p = rule.order_p;
+    res[i].n_eq = n_eq;
+    res[i].n_shape = nsh;
+    res[i].data.assign(out.begin() + i * kk, out.begin() + (i + 1) * kk);
+  }
+  return res;
 }
 
 /// run_batch-shaped entry (kernels.hpp:73-75): builds the rule and table like

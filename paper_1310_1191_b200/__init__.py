@@ -31,7 +31,7 @@ __all__ = [
     "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
     "generate_box_mesh", "generate_cdr_coefficients", "generate_materials", "laplace_tensor",
-    "Integrator", "run_batch", "measure_fp64_peak", "PRISTIF1", "PRISTIF2", "save_stiffness", "load_stiffness",
+    "Integrator", "run_batch", "integrate_host_multi", "measure_fp64_peak", "PRISTIF1", "PRISTIF2", "save_stiffness", "load_stiffness",
     "stiffness_info", "flops_dense_per_element", "bytes_per_element", "library",
 ]
 
@@ -139,6 +139,8 @@ def library():
     L.pi_integrate.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, C.c_int,
                                C.c_int64, vp, E]
     L.pi_integrate_f32.argtypes = L.pi_integrate.argtypes
+    L.pi_integrate_host_multi.argtypes = [C.POINTER(vp), C.c_int, C.c_int64, C.c_int64, vp, C.c_int, vp, vp,
+                                          C.c_int64, E]
     L.pi_load_vectors.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_double, vp, vp, E]
     L.pi_check.argtypes = [vp, E]
     L.pi_integrate_host.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int, vp, vp, C.c_int64, E]
@@ -435,6 +437,29 @@ class Integrator:
                                          _addr(out), chunk_elems, C.byref(err))
         _raise(st, err)
         return out
+
+
+def integrate_host_multi(integrators, geoms, coeff_mode=LAPLACE, coeff=None, element_id_base=0, out=None,
+                         chunk_elems=0):
+    """pi_integrate_host_multi: contiguous element ranges over several contexts
+    (one per GPU), one host thread each; bitwise equal to a single context."""
+    its = list(integrators)
+    geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
+    n = len(geoms)
+    dim = its[0].dim
+    if out is None:
+        out = np.empty((n, dim, dim))
+    cbuf = None
+    if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
+        cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
+    elif coeff_mode in (PER_ELEMENT, ELASTICITY):
+        cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(n, -1)
+    handles = (C.c_void_p * len(its))(*[it._h.value for it in its])
+    err = _ErrInfo()
+    st = library().pi_integrate_host_multi(handles, len(its), n, element_id_base, _addr(geoms), coeff_mode,
+                                           _addr(cbuf), _addr(out), chunk_elems, C.byref(err))
+    _raise(st, err)
+    return out
 
 
 def run_batch(p, mesh, coeff_mode=LAPLACE, coeff=None, device=0, **kw):

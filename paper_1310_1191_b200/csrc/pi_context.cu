@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -557,6 +558,50 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
     return st;
   }
   return PI_OK;
+}
+
+pi_status pi_integrate_host_multi(pi_context* const* ctxs, int n_ctx, int64_t n_elem, int64_t element_id_base,
+                                  const double* geom_aos, int coeff_mode, const double* coeff, double* out,
+                                  int64_t chunk_elems, pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctxs || n_ctx < 1) return set_error(err, PI_E_CONTRACT, "pi_integrate_host_multi: no contexts");
+  for (int g = 0; g < n_ctx; ++g) {
+    if (!ctxs[g]) return set_error(err, PI_E_CONTRACT, "pi_integrate_host_multi: NULL context %d", g);
+    if (ctxs[g]->p != ctxs[0]->p || ctxs[g]->n_eq != ctxs[0]->n_eq)
+      return set_error(err, PI_E_CONFIG, "pi_integrate_host_multi: contexts disagree on (p, n_eq)");
+    for (int h = 0; h < g; ++h)
+      if (ctxs[h] == ctxs[g]) return set_error(err, PI_E_CONTRACT, "pi_integrate_host_multi: context %d repeated", g);
+  }
+  if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
+  const int ne = ctxs[0]->n_eq;
+  const int64_t dim = static_cast<int64_t>(ctxs[0]->n_shape) * ne, kk = dim * dim;
+  // per-element coefficient stride (uniform modes share one buffer)
+  const int64_t cw = coeff_mode == PI_COEFF_PER_ELEMENT ? 16 * ne * ne : coeff_mode == PI_COEFF_ELASTICITY ? 2 : 0;
+  std::vector<pi_status> st(n_ctx, PI_OK);
+  std::vector<pi_error_info> errs(n_ctx);
+  auto work = [&](int g) {
+    // contiguous element range of context g (partition.py)
+    const int64_t lo = n_elem * g / n_ctx, hi = n_elem * (g + 1) / n_ctx;
+    if (hi <= lo) return;
+    st[g] = pi_integrate_host(ctxs[g], hi - lo, element_id_base + lo, geom_aos + 18 * lo, coeff_mode,
+                              coeff ? coeff + cw * lo : nullptr, out + kk * lo, chunk_elems, &errs[g]);
+  };
+  std::vector<std::thread> pool;
+  for (int g = 1; g < n_ctx; ++g) pool.emplace_back(work, g);
+  work(0);
+  for (auto& t : pool) t.join();
+  // report like a single call would: the lowest inverted element, else the first failure
+  int pick = -1;
+  for (int g = 0; g < n_ctx; ++g) {
+    if (st[g] == PI_OK) continue;
+    if (pick < 0) pick = g;
+    if (st[g] == PI_E_INVERTED_ELEMENT &&
+        (st[pick] != PI_E_INVERTED_ELEMENT || errs[g].element < errs[pick].element))
+      pick = g;
+  }
+  if (pick < 0) return PI_OK;
+  if (err) *err = errs[pick];
+  return st[pick];
 }
 
 double pi_flops_dense_per_element(int p, int n_eq, int coeff_mode) {

@@ -78,6 +78,22 @@ int main() {
     std::printf("p=%d elasticity vs integrate_optimized: %.3e\n", p, worst);
     if (!(worst <= 1e-12)) ++failures;
   }
+  // several contexts (one per device; here twice the same GPU): bitwise equal
+  {
+    const int p = 4;
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    CoefficientTensor lap = CoefficientTensor::zeros(1);
+    for (int d = 1; d <= 3; ++d) lap.set(0, 0, d, d, 1.0);
+    const auto one = prism_b200::integrate_batch(mesh, std::span<const CoefficientTensor>(&lap, 1), shapes, rule);
+    const int devs[3] = {0, 0, 0};
+    const auto multi = prism_b200::integrate_batch_multi(mesh, std::span<const CoefficientTensor>(&lap, 1), shapes,
+                                                         rule, std::span<const int>(devs, 3));
+    bool same = one.size() == multi.size();
+    for (size_t e = 0; same && e < one.size(); ++e) same = one[e].data == multi[e].data;
+    std::printf("integrate_batch_multi (3 contexts) bitwise equal: %s\n", same ? "yes" : "NO");
+    if (!same) ++failures;
+  }
   // error mapping: inverted element with batch offset, table mismatch
   {
     auto bad = generate_box_mesh(2, 2, 1, 0.0);
