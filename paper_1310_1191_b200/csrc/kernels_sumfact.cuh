@@ -82,6 +82,10 @@ struct SumFactLaunch;
 #ifdef PI_SF_OVERRIDE
 #include PI_SF_OVERRIDE
 #endif
+#ifndef PI_SF_NBUF
+#define PI_SF_NBUF 3
+#endif
+static_assert(PI_SF_NBUF >= 2 && PI_SF_NBUF <= 6, "named barriers: FULL/EMPTY per buffer + 2 <= 16");
 #ifndef PI_SF_2_1
 #define PI_SF_2_1 true, 8, 3, 3, 1, 3, 3, 4, 1, 1, 1
 #endif
@@ -172,7 +176,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static_assert(NTILE % (L::NB * L::NCB) == 0, "n-tiles must split evenly");
   // H for one chunk: [EPC][AG][4 s][NVE b'][3 x][4 y (padded)]
   static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NVE * 12;
-  static constexpr int NBUF = 3;  // H ring depth (producers run up to NBUF chunks ahead)
+  static constexpr int NBUF = PI_SF_NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
   // Scalar forms build M for every point of the item up front (one wide,
   // latency-bound pass instead of one per chunk); systems (9 blocks per
   // point) build it per chunk of 4 triangle points.
@@ -219,7 +223,9 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-constexpr int kBarFull0 = 1, kBarEmpty0 = 4, kBarProd = 7, kBarCons = 8;  // FULL/EMPTY: 3 ids each
+// named barrier ids: FULL and EMPTY per ring buffer, producers, consumers
+constexpr int kBarFull0 = 1, kBarEmpty0 = 1 + PI_SF_NBUF, kBarProd = 1 + 2 * PI_SF_NBUF,
+              kBarCons = 2 + 2 * PI_SF_NBUF;
 
 // Release fence for the shared-memory hand-off before bar.arrive (MEMBAR.ALL.CTA).
 __device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
@@ -250,13 +256,22 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // ---- per-p tables: staged once per (persistent) CTA ----
-  for (int i = tid; i < C::XFRAG; i += C::NTHREADS) sXA[i] = tab.xfrag[i];
-  for (int i = tid; i < C::XPLAIN; i += C::NTHREADS) sXP[i] = tab.xplain[i];
-  for (int i = tid; i < 2 * NV * NZ + NZ; i += C::NTHREADS) sY[i] = tab.yline[i];
-  for (int i = tid; i < 2 * NS; i += C::NTHREADS) sTri[i] = tab.tri[i];
-  for (int i = tid; i < NQ; i += C::NTHREADS) sW[i] = tab.w[i];
+  // ---- per-p tables: staged once per (persistent) CTA by TMA bulk copies ----
+  // (contiguous device arrays, sizes padded to 16 bytes by the host)
+  __shared__ __align__(8) uint64_t s_tables;
+  if (tid == 0) mbar_init(&s_tables, 1);
   __syncthreads();
+  if (tid == 0) {
+    constexpr unsigned BX = 8u * C::XFRAG, BP = 8u * C::XPLAIN, BY = 8u * ((2 * NV * NZ + NZ + 1) / 2 * 2),
+                       BT = 8u * 2 * NS, BW = 8u * ((NQ + 1) / 2 * 2);
+    mbar_arrive_expect_tx(&s_tables, BX + BP + BY + BT + BW);
+    bulk_load(sXA, tab.xfrag, BX, &s_tables);
+    bulk_load(sXP, tab.xplain, BP, &s_tables);
+    bulk_load(sY, tab.yline, BY, &s_tables);
+    bulk_load(sTri, tab.tri, BT, &s_tables);
+    bulk_load(sW, tab.w, BW, &s_tables);
+  }
+  mbar_wait(&s_tables, 0);
 
   const double* Pv = sY;            // P_a(z)  [NZ][NV]
   const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]

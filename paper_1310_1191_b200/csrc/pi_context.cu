@@ -137,7 +137,11 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaStreamCreate"));
   if ((st = upload(&ctx->d_phi, ctx->h_phi, err)) != PI_OK) return fail(st);
   if ((st = upload(&ctx->d_pts, ctx->h_pts, err)) != PI_OK) return fail(st);
-  if ((st = upload(&ctx->d_w, ctx->h_w, err)) != PI_OK) return fail(st);
+  {
+    std::vector<double> wpad(ctx->h_w);  // padded to 16 bytes for TMA bulk copies
+    wpad.resize((wpad.size() + 1) / 2 * 2, 0.0);
+    if ((st = upload(&ctx->d_w, wpad, err)) != PI_OK) return fail(st);
+  }
   ce = cudaMalloc(&ctx->d_bad, sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMalloc"));
   ce = cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long));

@@ -67,6 +67,7 @@ struct SumFactHost {
         yl[NV * NZ + z * NV + a] = PHI(z * NS, 3, a);
       }
     for (int z = 0; z < NZ; ++z) yl[2 * NV * NZ + z] = pts[3 * z * NS + 2];
+    yl.resize((yl.size() + 1) / 2 * 2, 0.0);  // 16-byte multiple for the TMA bulk copy
     // X_x(t,s): x=0 dm/dxi1, 1 dm/dxi2, 2 m, read at a=0 (P_0 = 1), z=0.
     std::vector<double> X(static_cast<size_t>(3) * NT * NS);
     for (int t = 0; t < NT; ++t)
