@@ -6,6 +6,11 @@
 
 #include "../../include/prism_b200.h"
 
+// A/B builds (tools/ab_build.sh): build-time overrides of launch shapes and switches.
+#ifdef PI_SF_OVERRIDE
+#include PI_SF_OVERRIDE
+#endif
+
 namespace pib {
 
 // Per-launch arguments common to every strategy.
@@ -319,10 +324,12 @@ __device__ __forceinline__ void flag_inverted(unsigned long long* bad, int64_t g
 // D = A(8x4) * B(4x8) + D, FP64 tensor core (SASS DMMA.8x8x4).
 // Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 // d0,d1 = D[lane/4][2*(lane%4) + {0,1}].
+// Not volatile: the MMA is a pure function of its operands, so the compiler
+// may schedule independent MMAs and their operand arithmetic freely.
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
 }
 
 }  // namespace pib

@@ -78,10 +78,7 @@ template <int P, int NE>
 struct SumFactLaunch;
 // Per (p, n_eq): TMAJOR, EPC, AG, WA, NG, NBB, NB, NPW, BSPLIT, MINB, NCB.
 // Each can be overridden at build time (A/B runs, tools/ab_build.sh): a header
-// named by -DPI_SF_OVERRIDE defining PI_SF_<p>_<n_eq>.
-#ifdef PI_SF_OVERRIDE
-#include PI_SF_OVERRIDE
-#endif
+// named by -DPI_SF_OVERRIDE (included by kernels_common.cuh) defining PI_SF_<p>_<n_eq>.
 #ifndef PI_SF_NBUF
 #define PI_SF_NBUF 3
 #endif
