@@ -29,7 +29,13 @@ __constant__ double c_pts_e1[kE1NQ * 4];           // xi1, xi2, xi3, w
 
 constexpr int kE1Warps = 3;
 constexpr int kE1Pitch = kE1KK + 1;  // odd pitch: staged elements hit distinct banks
-constexpr int kE1Round = 8;          // elements staged per output round
+#ifndef PI_E1_ROUND
+#define PI_E1_ROUND 16
+#endif
+#ifndef PI_E1_MINB
+#define PI_E1_MINB 4
+#endif
+constexpr int kE1Round = PI_E1_ROUND;  // elements staged per output round
 constexpr int kE1NG = 20;            // per point: g_d(i) (18), dw*lam, dw*mu
 struct E1Smem {
   static constexpr int GBUF = kE1NQ * kE1NG * 32;
@@ -112,7 +118,7 @@ __device__ __forceinline__ void e1_store(T* st, int64_t ld, const double* acc) {
     default: CALL(2); break; \
   }
 
-__global__ void __launch_bounds__(32 * kE1Warps, 4) p1_elastic_lane_kernel(LaunchArgs args) {
+__global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_kernel(LaunchArgs args) {
   using BP = BasisPattern<1>;
   constexpr int NACC = 57;
   extern __shared__ __align__(16) double e1_smem[];

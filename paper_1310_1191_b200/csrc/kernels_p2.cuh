@@ -43,7 +43,14 @@ struct P2Cfg {
   static constexpr int NACC = SYM ? kP2NSH + 1 : kP2NSH;
   static constexpr int NTHREADS = 32 * NW;
   static constexpr int NM = GENERAL ? 16 : 6;            // stored M entries per point
-  static constexpr int ROUND = SYM ? 8 : 16;             // elements staged per output round
+#ifndef PI_P2_ROUND_SYM
+#define PI_P2_ROUND_SYM 32
+#endif
+#ifndef PI_P2_ROUND_GEN
+#define PI_P2_ROUND_GEN 32
+#endif
+  // elements staged per output round (32: the whole group, one round)
+  static constexpr int ROUND = SYM ? PI_P2_ROUND_SYM : PI_P2_ROUND_GEN;
   static constexpr int MBUF = kP2NQ * NM * 32;           // doubles
   static constexpr int SBUF = ROUND * kP2Pitch;
   static constexpr int BUF = MBUF > SBUF ? MBUF : SBUF;
