@@ -171,8 +171,43 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int RC = R < L::NB ? R : L::NB;     // distinct b' values a lane touches
   static_assert(S::NVE % L::AG == 0 && L::AG % L::WA == 0, "bad a-grouping");
   static_assert(NTILE % (L::NB * L::NCB) == 0, "n-tiles must split evenly");
-  // H for one chunk: [EPC][AG][4 s][NVE b'][3 x][4 y (padded)]
-  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * S::NVE * 12;
+  // H for one chunk: [EPC][AG][4 s (stride HS)][NVE b' (stride HB)][3 x][4 y (padded)].
+  // HB and HS are padded so that the natural-order consumers' 16-byte H loads
+  // (a quarter warp = 2 consecutive b' x 4 (s, x) pairs) hit distinct bank
+  // groups: chosen at compile time by counting conflicts (hconflicts).
+  static constexpr int hconflicts(int hb, int hs) {
+    int worst = 0;
+    for (int ks = 0; ks < 3; ++ks)
+      for (int nb = 0; nb < (NTILE < 8 ? NTILE : 8); ++nb)
+        for (int q = 0; q < 4; ++q) {
+          int offs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, n = 0;
+          for (int l = 0; l < 8; ++l) {
+            const int lane = 8 * q + l, kk = 4 * ks + (lane & 3);
+            const int b = (nb * 8 + (lane >> 2)) % S::NVE;
+            const int off = (kk / 3) * hs + b * hb + (kk % 3) * 4;
+            bool seen = false;
+            for (int i = 0; i < n; ++i) seen = seen || offs[i] == off;
+            if (!seen) offs[n++] = off;
+          }
+          int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int i = 0; i < n; ++i) ++cnt[(offs[i] / 2) % 8];
+          for (int g = 0; g < 8; ++g) worst = worst > cnt[g] ? worst : cnt[g];
+        }
+    return worst;
+  }
+  static constexpr int hpick() {  // returns hb * 1024 + hs
+    int best = 1 << 30, pick = 12 * 1024 + S::NVE * 12;
+    for (int hb = 12; hb <= 18; hb += 2)
+      for (int pad = 0; pad < 16; pad += 2) {
+        const int hs = S::NVE * hb + pad;
+        const int score = hconflicts(hb, hs) * 100000 + hs;  // fewest conflicts, then least memory
+        if (score < best) best = score, pick = hb * 1024 + hs;
+      }
+    return pick;
+  }
+  static constexpr int HB = L::TMAJOR ? 12 : hpick() / 1024;
+  static constexpr int HS = L::TMAJOR ? S::NVE * 12 : hpick() % 1024;
+  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * HS;
   static constexpr int NBUF = PI_SF_NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
   // Scalar forms build M for every point of the item up front (one wide,
   // latency-bound pass instead of one per chunk); systems (9 blocks per
@@ -406,7 +441,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           for (int bb = 0; bb < C::BPER; ++bb) {
             const int bp = bg * C::BPER + bb;
             if (bp < NVE) {
-              double* dst = Hb + ((((el * AG + al) * 4 + sl) * NVE + bp) * 3 + x) * 4;
+              double* dst = Hb + ((el * AG + al) * 4 + sl) * C::HS + bp * C::HB + x * 4;
               *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
               dst[2] = h[bb][2];
             }
@@ -461,7 +496,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
       // when NCB == 1, so b' and t' are resolved per item below for NCB > 1.
       const int j = ntl0[nb] * 8 + cpos;
       const int tp = j / NVE, b = j - tp * NVE;
-      hoff[nb] = b * 12;  // + x*4 at use
+      hoff[nb] = b * C::HB;  // + x*4 at use
       xoff0[nb] = tp;     // + s*3*NTPS at use
       const int tmax = min(NT - 1, (ntl0[nb] * 8 + 7) / NVE);
       unsigned m = 0;
@@ -523,11 +558,11 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + ((((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NVE) * 3 + x_k[ks]) * 4;
+            const double* Hs = Hb + ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS + x_k[ks] * 4;
 #pragma unroll
             for (int b = 0; b < NVE; ++b) {
-              const double2 h01 = *reinterpret_cast<const double2*>(Hs + b * 12);
-              const double h2 = Hs[b * 12 + 2];
+              const double2 h01 = *reinterpret_cast<const double2*>(Hs + b * C::HB);
+              const double h2 = Hs[b * C::HB + 2];
 #pragma unroll
               for (int g = 0; g < MT; ++g) {
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
@@ -552,7 +587,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + (((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * NVE) * 12 + x_k[ks] * 4;
+            const double* Hs = Hb + ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS + x_k[ks] * 4;
             // b' for n-tile nb is b'_(nb mod R): load each distinct one once
             double hr[C::RC][3];
 #pragma unroll
