@@ -195,18 +195,37 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
         }
     return worst;
   }
+  // producers' 16-byte H stores: quarter warps of consecutive items (b'-group, x, s, ...)
+  static constexpr int pconflicts(int hb, int hs) {
+    int worst = 0;
+    constexpr int items = L::EPC * L::AG * 4 * 3 * L::BSPLIT;
+    for (int q0 = 0; q0 < items; q0 += 8)
+      for (int bb = 0; bb < BPER; ++bb) {
+        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = q0; i < q0 + 8 && i < items; ++i) {
+          const int bg = i % L::BSPLIT, x = (i / L::BSPLIT) % 3, sl = (i / (3 * L::BSPLIT)) % 4;
+          const int alg = i / (12 * L::BSPLIT);  // (el, al)
+          const int off = alg * 4 * hs + sl * hs + (bg * BPER + bb) * hb + x * 4;
+          ++cnt[(off / 2) % 8];
+        }
+        for (int g = 0; g < 8; ++g) worst = worst > cnt[g] ? worst : cnt[g];
+      }
+    return worst;
+  }
   static constexpr int hpick() {  // returns hb * 1024 + hs
     int best = 1 << 30, pick = 12 * 1024 + S::NVE * 12;
     for (int hb = 12; hb <= 18; hb += 2)
       for (int pad = 0; pad < 16; pad += 2) {
         const int hs = S::NVE * hb + pad;
-        const int score = hconflicts(hb, hs) * 100000 + hs;  // fewest conflicts, then least memory
+        // t'-major consumers read H warp-uniformly in b': only the stores matter there
+        const int cons = L::TMAJOR ? 1 : hconflicts(hb, hs);
+        const int score = cons * 10000000 + pconflicts(hb, hs) * 10000 + hs;  // then least memory
         if (score < best) best = score, pick = hb * 1024 + hs;
       }
     return pick;
   }
-  static constexpr int HB = L::TMAJOR ? 12 : hpick() / 1024;
-  static constexpr int HS = L::TMAJOR ? S::NVE * 12 : hpick() % 1024;
+  static constexpr int HB = hpick() / 1024;
+  static constexpr int HS = hpick() % 1024;
   static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * HS;
   static constexpr int NBUF = PI_SF_NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
   // Scalar forms build M for every point of the item up front (one wide,
