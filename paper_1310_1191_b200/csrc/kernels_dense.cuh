@@ -19,7 +19,12 @@ struct DenseTables {
   const double* w;    // [NQ]
 };
 
-constexpr int kP1Threads = 128;
+// threads (= elements) per CTA: 128 for Laplace; 64 for general tensors,
+// whose 2 resident CTAs/SM then interleave their load and compute phases better
+template <bool GENERAL>
+constexpr int p1_threads() {
+  return GENERAL ? 64 : 128;
+}
 #ifndef PI_P1_MINB_GENERAL
 #define PI_P1_MINB_GENERAL 2
 #endif
@@ -49,7 +54,9 @@ struct BasisPattern {
 // skipped at compile time (13 of the 24 phi entries per point are non-zero),
 // so the contraction costs about half the dense loop nest's FMAs.
 template <bool GENERAL>
-__global__ void __launch_bounds__(kP1Threads, GENERAL ? PI_P1_MINB_GENERAL : 4) p1_thread_kernel(LaunchArgs args, DenseTables tab) {
+__global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : 4)
+    p1_thread_kernel(LaunchArgs args, DenseTables tab) {
+  constexpr int kP1Threads = p1_threads<GENERAL>();
   constexpr int NQ = 6, NSH = 6, KK = NSH * NSH;
   using BP = BasisPattern<1>;
   __shared__ double sPhi[NQ * 4 * NSH];

@@ -217,3 +217,137 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
 #undef E1_WARP_SWITCH
 
 }  // namespace pib
+
+namespace pib {
+
+// ---------------------------------------------------------------------------
+// p = 2 isotropic elasticity (K 54x54): one warp per element, lanes own 3x3
+// blocks.  The 171 upper-triangle shape blocks (i, j >= i) are dealt to the
+// 32 lanes round-robin (5 or 6 blocks, 54 accumulators); per rule point a
+// lane reads the physical gradients g(i), g(j) of its blocks (computed once
+// per element into the warp's shared memory, structural zeros skipped) and
+// updates the 63-flop block of integrate_optimized.  The element matrix is
+// staged in the warp's shared memory (mirrors included) and leaves with
+// coalesced 16-byte stores.
+constexpr int kE2NQ = 18, kE2NSH = 18, kE2DIM = 54, kE2KK = kE2DIM * kE2DIM, kE2NBLK = 171;
+__constant__ double c_phi_e2[kE2NQ * 4 * kE2NSH];  // tabulate_shapes order [q][k][dof]
+__constant__ double c_pts_e2[kE2NQ * 4];           // xi1, xi2, xi3, w
+__constant__ unsigned char c_blk_e2[2 * 192];      // (i, j) of upper-triangle block b (padded)
+
+constexpr int kE2Warps = 4;
+constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
+constexpr int kE2G = kE2NQ * (kE2NSH * 3 + 2);     // per point: g_d(i) (54), dw*lam, dw*mu
+constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases the gradients
+constexpr size_t kE2SmemBytes = sizeof(double) * (kE2WarpDoubles + 2) * kE2Warps;
+
+__global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(LaunchArgs args) {
+  using BP = BasisPattern<2>;
+  extern __shared__ __align__(16) double e2_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sw = e2_smem + warp * (kE2WarpDoubles + 2);  // this warp's region (16-byte aligned)
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kE2Warps;
+  // the lane's blocks (i, j)
+  int bi[kE2BPL], bj[kE2BPL];
+#pragma unroll
+  for (int k = 0; k < kE2BPL; ++k) {
+    const int b = lane + 32 * k;
+    bi[k] = c_blk_e2[2 * b];
+    bj[k] = c_blk_e2[2 * b + 1];
+  }
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * kE2Warps + warp; e < args.n_elem; e += nwarps) {
+    // ---- geometry, material, then per-point gradients (lane = point) ----
+    double lam, mu;
+    {
+      const double young = args.coeff ? args.coeff[e] : args.cu[0];
+      const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+      lame(young, nu, lam, mu);
+    }
+    double x[18], d[21];
+#pragma unroll
+    for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e];  // warp-uniform (broadcast) loads
+    prism_edges(x, d);
+    bool inverted = false;
+    if (lane < kE2NQ) {
+      const int q = lane;
+      double cf[3][3];
+      const double det = jacobian_cofactors(d, c_pts_e2[4 * q], c_pts_e2[4 * q + 1], c_pts_e2[4 * q + 2], cf);
+      inverted = !(det > 0.0);
+      const double id = __drcp_rn(det), dw = det * c_pts_e2[4 * q + 3];
+      double* gq = sw + q * (kE2NSH * 3 + 2);
+#pragma unroll
+      for (int i = 0; i < kE2NSH; ++i)
+#pragma unroll
+        for (int dd = 0; dd < 3; ++dd) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (BP::nz(k + 1, i)) s = fma(c_phi_e2[(q * 4 + k + 1) * kE2NSH + i], cf[dd][k], s);
+          gq[i * 3 + dd] = s * id;
+        }
+      gq[kE2NSH * 3] = dw * lam;
+      gq[kE2NSH * 3 + 1] = dw * mu;
+    }
+    if (__any_sync(0xffffffffu, inverted) && lane == 0) flag_inverted(args.bad, args.element_id_base + e);
+    __syncwarp();
+    // ---- accumulate the lane's blocks over the rule points ----
+    double acc[kE2BPL][9];
+#pragma unroll
+    for (int k = 0; k < kE2BPL; ++k)
+#pragma unroll
+      for (int m = 0; m < 9; ++m) acc[k][m] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < kE2NQ; ++q) {
+      const double* gq = sw + q * (kE2NSH * 3 + 2);
+      const double l = gq[kE2NSH * 3], m_ = gq[kE2NSH * 3 + 1];
+#pragma unroll
+      for (int k = 0; k < kE2BPL; ++k) {
+        if (k == kE2BPL - 1 && lane + 32 * k >= kE2NBLK) break;  // lanes 11..31 own 5 blocks
+        const double* gi = gq + bi[k] * 3;
+        const double* gj = gq + bj[k] * 3;
+        const double a0 = gi[0], a1 = gi[1], a2 = gi[2], b0 = gj[0], b1 = gj[1], b2 = gj[2];
+        const double dot = m_ * fma(a0, b0, fma(a1, b1, a2 * b2));
+        const double la[3] = {l * a0, l * a1, l * a2}, ma[3] = {m_ * a0, m_ * a1, m_ * a2};
+        const double bb[3] = {b0, b1, b2};
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+          for (int je = 0; je < 3; ++je) {
+            double v = fma(la[ie], bb[je], fma(ma[je], bb[ie], acc[k][ie * 3 + je]));
+            if (ie == je) v += dot;
+            acc[k][ie * 3 + je] = v;
+          }
+      }
+    }
+    __syncwarp();  // gradients no longer read: the region becomes the staging of K
+    // ---- stage the element matrix (mirrors included), then coalesced stores ----
+#pragma unroll
+    for (int k = 0; k < kE2BPL; ++k) {
+      if (k == kE2BPL - 1 && lane + 32 * k >= kE2NBLK) break;
+#pragma unroll
+      for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+        for (int je = 0; je < 3; ++je) {
+          const int r = bi[k] * 3 + ie, c = bj[k] * 3 + je;
+          const double v = acc[k][ie * 3 + je];
+          if (bi[k] != bj[k] || ie <= je) {
+            sw[r * kE2DIM + c] = v;
+            sw[c * kE2DIM + r] = v;
+          }
+        }
+    }
+    __syncwarp();
+    if (args.out_layout == PI_OUT_SOA) {
+      for (int r = lane; r < kE2KK; r += 32) store_out(args, static_cast<int64_t>(r) * args.ld_out + e, sw[r]);
+    } else if (args.out32) {
+      for (int r = lane; r < kE2KK; r += 32) args.out32[e * kE2KK + r] = static_cast<float>(sw[r]);
+    } else {
+      // 2916 doubles per element: every element starts 16-byte aligned
+      double2* dst = reinterpret_cast<double2*>(args.out + e * kE2KK);
+      const double2* src = reinterpret_cast<const double2*>(sw);
+      for (int r = lane; r < kE2KK / 2; r += 32) dst[r] = src[r];
+    }
+    __syncwarp();  // staging read out before the next element's gradients overwrite it
+  }
+}
+
+}  // namespace pib

@@ -34,6 +34,7 @@ struct pi_context {
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
   int e1_ctas = 0;             // persistent grid of p1_elastic_lane_kernel
+  int e2_ctas = 0;             // persistent grid of p2_elastic_warp_kernel
   double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
@@ -75,7 +76,7 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
 
 int resolve_variant(const pi_context* ctx) {
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
-  if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p == 1)) return PI_VARIANT_DENSE;
+  if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p <= 2)) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
 
@@ -176,6 +177,14 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
+  if (p == 2 && n_eq == 3) {
+    cudaFuncSetAttribute(p2_elastic_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kE2SmemBytes));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2_elastic_warp_kernel, 32 * kE2Warps, kE2SmemBytes);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->e2_ctas = std::max(1, per_sm) * sms;
+  }
   if (p == 1 && n_eq == 3) {
     cudaFuncSetAttribute(p1_elastic_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(E1Smem::BYTES));
@@ -246,8 +255,8 @@ pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* er
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
-  if (variant == PI_VARIANT_DENSE && !((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p == 1)))
-    return set_error(err, PI_E_CONFIG, "dense variant is built for scalar forms at p <= 2 and elasticity at p = 1");
+  if (variant == PI_VARIANT_DENSE && ctx->p > 2)
+    return set_error(err, PI_E_CONFIG, "dense variant is built for p <= 2 only (scalar forms and elasticity)");
   ctx->variant = variant;
   return PI_OK;
 }
@@ -336,7 +345,28 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
   const int v = resolve_variant(ctx);
   const bool e1_lane = ne == 3 && ctx->p == 1 && v == PI_VARIANT_DENSE && form == kFormElasticity;
-  if (e1_lane) {
+  const bool e2_warp = ne == 3 && ctx->p == 2 && v == PI_VARIANT_DENSE && form == kFormElasticity;
+  if (e2_warp) {
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e2, ctx->d_phi, sizeof(double) * kE2NQ * 4 * kE2NSH, 0,
+                                    cudaMemcpyDeviceToDevice, s),
+            "upload p=2 shape table");
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_e2, ctx->d_pts4, sizeof(double) * kE2NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
+            "upload p=2 rule");
+    static const std::vector<unsigned char> blk = [] {
+      std::vector<unsigned char> t(2 * 192, 0);
+      int b = 0;
+      for (int i = 0; i < kE2NSH; ++i)
+        for (int j = i; j < kE2NSH; ++j, ++b) {
+          t[2 * b] = static_cast<unsigned char>(i);
+          t[2 * b + 1] = static_cast<unsigned char>(j);
+        }
+      return t;
+    }();
+    PI_CUDA(cudaMemcpyToSymbolAsync(c_blk_e2, blk.data(), blk.size(), 0, cudaMemcpyHostToDevice, s),
+            "upload p=2 block table");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + kE2Warps - 1) / kE2Warps, ctx->e2_ctas));
+    p2_elastic_warp_kernel<<<grid, 32 * kE2Warps, kE2SmemBytes, s>>>(a);
+  } else if (e1_lane) {
     PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e1, ctx->d_phi, sizeof(double) * kE1NQ * 4 * kE1NSH, 0,
                                     cudaMemcpyDeviceToDevice, s),
             "upload p=1 shape table");
@@ -361,11 +391,13 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
       p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
   } else if (v == PI_VARIANT_DENSE && ne == 1) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
-    const unsigned grid = static_cast<unsigned>((n_elem + kP1Threads - 1) / kP1Threads);
-    if (general)
-      p1_thread_kernel<true><<<grid, kP1Threads, 0, s>>>(a, t);
-    else
-      p1_thread_kernel<false><<<grid, kP1Threads, 0, s>>>(a, t);
+    if (general) {
+      constexpr int T = p1_threads<true>();
+      p1_thread_kernel<true><<<static_cast<unsigned>((n_elem + T - 1) / T), T, 0, s>>>(a, t);
+    } else {
+      constexpr int T = p1_threads<false>();
+      p1_thread_kernel<false><<<static_cast<unsigned>((n_elem + T - 1) / T), T, 0, s>>>(a, t);
+    }
   } else {
     SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
     sumfact_launch(ctx->p, ne, form, symmetric, a, t, s);
@@ -635,6 +667,11 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   // reciprocal ~6, M block 24 (Laplace) / ~100 (general), in FLOPs.
   const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
   const int v = resolve_variant(ctx);
+  if (v == PI_VARIANT_DENSE && ctx->n_eq == 3 && p == 2) {
+    // p2_elastic_warp_kernel: per point 18 gradient triples (about 2 FMA each),
+    // then 171 blocks x (3-FMA dot + 9 x 2 FMA + 6 scalings)
+    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 18 * 3 * 2 + 2.0 * 171 * (3 + 18 + 6));
+  }
   if (v == PI_VARIANT_DENSE && ctx->n_eq == 3) {
     // p1_elastic_lane_kernel: Jacobian/cofactors, 18 physical gradients
     // (7 structural non-zeros x 3), then 3 warps x (57 entries x 2 FMA +
