@@ -238,13 +238,18 @@ constexpr int kE2Warps = 4;
 constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
 constexpr int kE2G = kE2NQ * (kE2NSH * 3 + 2);     // per point: g_d(i) (54), dw*lam, dw*mu
 constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases the gradients
-constexpr size_t kE2SmemBytes = sizeof(double) * (kE2WarpDoubles + 2) * kE2Warps;
+constexpr int kE2Phi = kE2NQ * 4 * kE2NSH;          // the shape table, staged per CTA
+constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
 
 __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(LaunchArgs args) {
   using BP = BasisPattern<2>;
   extern __shared__ __align__(16) double e2_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sw = e2_smem + warp * (kE2WarpDoubles + 2);  // this warp's region (16-byte aligned)
+  // lanes read the table at different points: shared memory, not the constant bank
+  double* sPhi = e2_smem + (kE2WarpDoubles + 2) * kE2Warps;
+  for (int i = threadIdx.x; i < kE2Phi; i += 32 * kE2Warps) sPhi[i] = c_phi_e2[i];
+  __syncthreads();
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kE2Warps;
   // the lane's blocks (i, j)
   int bi[kE2BPL], bj[kE2BPL];
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
           double s = 0.0;
 #pragma unroll
           for (int k = 0; k < 3; ++k)
-            if (BP::nz(k + 1, i)) s = fma(c_phi_e2[(q * 4 + k + 1) * kE2NSH + i], cf[dd][k], s);
+            if (BP::nz(k + 1, i)) s = fma(sPhi[(q * 4 + k + 1) * kE2NSH + i], cf[dd][k], s);
           gq[i * 3 + dd] = s * id;
         }
       gq[kE2NSH * 3] = dw * lam;
