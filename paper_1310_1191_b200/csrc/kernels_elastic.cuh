@@ -356,3 +356,143 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
 }
 
 }  // namespace pib
+
+namespace pib {
+
+// ---------------------------------------------------------------------------
+// p = 3 isotropic elasticity (K 120x120): one CTA (4 warps) per element.  The
+// 820 upper-triangle 3x3 shape blocks are dealt to the 128 threads
+// round-robin (6-7 blocks, 63 accumulators).  Inverse Jacobians of the 48
+// rule points, then the 40 x 3 physical gradients per point are computed
+// into shared memory by the whole CTA; the block form is the 63-flop one of
+// integrate_optimized.  K is 115 KB per element, so blocks are stored
+// straight from registers (3-double row segments, the mirrored block
+// transposed); the CTA's writes to one element merge in L2.
+constexpr int kE3NQ = 48, kE3NSH = 40, kE3DIM = 120, kE3KK = kE3DIM * kE3DIM, kE3NBLK = 820;
+constexpr int kE3Threads = 128, kE3BPT = (kE3NBLK + kE3Threads - 1) / kE3Threads;  // 7
+constexpr int kE3GP = kE3NSH * 3 + 2;  // per point: g_d(i), dw*lam, dw*mu
+struct E3Smem {  // the 61 KB shape table is read through L1 (read-only loads), not staged
+  static constexpr int OFF_PTS = 0;                                // [NQ][4]
+  static constexpr int OFF_INV = OFF_PTS + kE3NQ * 4;              // [NQ][10]: inverse, dw
+  static constexpr int OFF_G = OFF_INV + kE3NQ * 10;               // [NQ][GP]
+  static constexpr int DOUBLES = OFF_G + kE3NQ * kE3GP;
+  static constexpr size_t BYTES = DOUBLES * sizeof(double);
+};
+
+__global__ void __launch_bounds__(kE3Threads, 2) p3_elastic_cta_kernel(LaunchArgs args, DenseTables tab) {
+  extern __shared__ __align__(16) double e3_smem[];
+  double* sPts = e3_smem + E3Smem::OFF_PTS;
+  double* sInv = e3_smem + E3Smem::OFF_INV;
+  double* sG = e3_smem + E3Smem::OFF_G;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < kE3NQ; q += kE3Threads) {
+    sPts[4 * q] = tab.pts[3 * q];
+    sPts[4 * q + 1] = tab.pts[3 * q + 1];
+    sPts[4 * q + 2] = tab.pts[3 * q + 2];
+    sPts[4 * q + 3] = tab.w[q];
+  }
+  // this thread's blocks (i, j >= i), upper-triangle enumeration b -> (i, j)
+  int bi[kE3BPT], bj[kE3BPT];
+#pragma unroll
+  for (int k = 0; k < kE3BPT; ++k) {
+    int b = tid + kE3Threads * k, i = 0;
+    if (b >= kE3NBLK) b = kE3NBLK - 1;
+    while (b >= kE3NSH - i) b -= kE3NSH - i++;
+    bi[k] = i;
+    bj[k] = i + b;
+  }
+  __syncthreads();
+  for (int64_t e = blockIdx.x; e < args.n_elem; e += gridDim.x) {
+    double lam, mu;
+    {
+      const double young = args.coeff ? args.coeff[e] : args.cu[0];
+      const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+      lame(young, nu, lam, mu);
+    }
+    // (1) inverse Jacobian and dw per point (threads 0..47)
+    bool inverted = false;
+    if (tid < kE3NQ) {
+      double x[18], d[21];
+#pragma unroll
+      for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e];
+      prism_edges(x, d);
+      const int q = tid;
+      double cf[3][3];
+      const double det = jacobian_cofactors(d, sPts[4 * q], sPts[4 * q + 1], sPts[4 * q + 2], cf);
+      inverted = !(det > 0.0);
+      const double id = __drcp_rn(det);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int dd = 0; dd < 3; ++dd) sInv[q * 10 + k * 3 + dd] = cf[dd][k] * id;  // inv[k][dd]
+      sInv[q * 10 + 9] = det * sPts[4 * q + 3];
+    }
+    if (__syncthreads_or(inverted) && tid == 0) flag_inverted(args.bad, args.element_id_base + e);
+    // (2) gradients g_d(i) at every point, (q, i) pairs over the CTA
+    for (int t = tid; t < kE3NQ * kE3NSH; t += kE3Threads) {
+      const int q = t / kE3NSH, i = t - q * kE3NSH;
+      const double* ph = tab.phi + q * 4 * kE3NSH + i;
+      const double f1 = __ldg(ph + kE3NSH), f2 = __ldg(ph + 2 * kE3NSH), f3 = __ldg(ph + 3 * kE3NSH);
+      const double* inv = sInv + q * 10;
+      double* g = sG + q * kE3GP + i * 3;
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) g[dd] = fma(f1, inv[dd], fma(f2, inv[3 + dd], f3 * inv[6 + dd]));
+    }
+    for (int q = tid; q < kE3NQ; q += kE3Threads) {
+      sG[q * kE3GP + kE3NSH * 3] = sInv[q * 10 + 9] * lam;
+      sG[q * kE3GP + kE3NSH * 3 + 1] = sInv[q * 10 + 9] * mu;
+    }
+    __syncthreads();
+    // (3) accumulate the thread's blocks
+    double acc[kE3BPT][9];
+#pragma unroll
+    for (int k = 0; k < kE3BPT; ++k)
+#pragma unroll
+      for (int m = 0; m < 9; ++m) acc[k][m] = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < kE3NQ; ++q) {
+      const double* gq = sG + q * kE3GP;
+      const double l = gq[kE3NSH * 3], m_ = gq[kE3NSH * 3 + 1];
+#pragma unroll
+      for (int k = 0; k < kE3BPT; ++k) {
+        const double* gi = gq + bi[k] * 3;
+        const double* gj = gq + bj[k] * 3;
+        const double a0 = gi[0], a1 = gi[1], a2 = gi[2], b0 = gj[0], b1 = gj[1], b2 = gj[2];
+        const double dot = m_ * fma(a0, b0, fma(a1, b1, a2 * b2));
+        const double la[3] = {l * a0, l * a1, l * a2}, ma[3] = {m_ * a0, m_ * a1, m_ * a2};
+        const double bb[3] = {b0, b1, b2};
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+          for (int je = 0; je < 3; ++je) {
+            double v = fma(la[ie], bb[je], fma(ma[je], bb[ie], acc[k][ie * 3 + je]));
+            if (ie == je) v += dot;
+            acc[k][ie * 3 + je] = v;
+          }
+      }
+    }
+    // (4) store the blocks (and their mirrors) straight from registers
+#pragma unroll
+    for (int k = 0; k < kE3BPT; ++k) {
+      if (tid + kE3Threads * k >= kE3NBLK) break;
+#pragma unroll
+      for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+        for (int je = 0; je < 3; ++je) {
+          const int r = bi[k] * 3 + ie, c = bj[k] * 3 + je;
+          if (bi[k] == bj[k] && ie > je) continue;
+          const double v = acc[k][ie * 3 + je];
+          if (args.out_layout == PI_OUT_SOA) {
+            store_out(args, static_cast<int64_t>(r * kE3DIM + c) * args.ld_out + e, v);
+            if (r != c) store_out(args, static_cast<int64_t>(c * kE3DIM + r) * args.ld_out + e, v);
+          } else {
+            store_out(args, e * kE3KK + r * kE3DIM + c, v);
+            if (r != c) store_out(args, e * kE3KK + c * kE3DIM + r, v);
+          }
+        }
+    }
+    __syncthreads();  // gradients read before the next element overwrites them
+  }
+}
+
+}  // namespace pib

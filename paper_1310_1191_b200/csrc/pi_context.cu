@@ -35,6 +35,7 @@ struct pi_context {
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
   int e1_ctas = 0;             // persistent grid of p1_elastic_lane_kernel
   int e2_ctas = 0;             // persistent grid of p2_elastic_warp_kernel
+  int e3_ctas = 0;             // persistent grid of p3_elastic_cta_kernel
   double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
   unsigned long long* d_bad = nullptr;
   std::vector<CallRecord> calls;
@@ -76,7 +77,7 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
 
 int resolve_variant(const pi_context* ctx) {
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
-  if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p <= 2)) return PI_VARIANT_DENSE;
+  if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p <= 3)) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
 }
 
@@ -177,6 +178,14 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
+  if (p == 3 && n_eq == 3) {
+    cudaFuncSetAttribute(p3_elastic_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(E3Smem::BYTES));
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p3_elastic_cta_kernel, kE3Threads, E3Smem::BYTES);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctx->e3_ctas = std::max(1, per_sm) * sms;
+  }
   if (p == 2 && n_eq == 3) {
     cudaFuncSetAttribute(p2_elastic_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kE2SmemBytes));
@@ -255,8 +264,8 @@ pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* er
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
-  if (variant == PI_VARIANT_DENSE && ctx->p > 2)
-    return set_error(err, PI_E_CONFIG, "dense variant is built for p <= 2 only (scalar forms and elasticity)");
+  if (variant == PI_VARIANT_DENSE && ctx->p > (ctx->n_eq == 3 ? 3 : 2))
+    return set_error(err, PI_E_CONFIG, "dense variant is built for scalar forms at p <= 2 and elasticity at p <= 3");
   ctx->variant = variant;
   return PI_OK;
 }
@@ -346,7 +355,12 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   const int v = resolve_variant(ctx);
   const bool e1_lane = ne == 3 && ctx->p == 1 && v == PI_VARIANT_DENSE && form == kFormElasticity;
   const bool e2_warp = ne == 3 && ctx->p == 2 && v == PI_VARIANT_DENSE && form == kFormElasticity;
-  if (e2_warp) {
+  const bool e3_cta = ne == 3 && ctx->p == 3 && v == PI_VARIANT_DENSE && form == kFormElasticity;
+  if (e3_cta) {
+    DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_elem, ctx->e3_ctas));
+    p3_elastic_cta_kernel<<<grid, kE3Threads, E3Smem::BYTES, s>>>(a, t);
+  } else if (e2_warp) {
     PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e2, ctx->d_phi, sizeof(double) * kE2NQ * 4 * kE2NSH, 0,
                                     cudaMemcpyDeviceToDevice, s),
             "upload p=2 shape table");
@@ -667,6 +681,11 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   // reciprocal ~6, M block 24 (Laplace) / ~100 (general), in FLOPs.
   const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
   const int v = resolve_variant(ctx);
+  if (v == PI_VARIANT_DENSE && ctx->n_eq == 3 && p == 3) {
+    // p3_elastic_cta_kernel: inverse per point, 40 gradient triples (9 FMA each),
+    // 820 blocks x (3-FMA dot + 9 x 2 FMA + 6 scalings)
+    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 40 * 9 + 2.0 * 820 * (3 + 18 + 6));
+  }
   if (v == PI_VARIANT_DENSE && ctx->n_eq == 3 && p == 2) {
     // p2_elastic_warp_kernel: per point 18 gradient triples (about 2 FMA each),
     // then 171 blocks x (3-FMA dot + 9 x 2 FMA + 6 scalings)
