@@ -2,7 +2,8 @@
 //
 // A tiny extern "C" face over the UNMODIFIED reference sources
 // (/root/reference/proj/src/{errors,reference_element,geometry,coefficients,
-// integrate_ref}.cpp), compiled together by oracle/Makefile into
+// integrate_ref}.cpp, plus io.cpp when nlohmann json is available), compiled
+// together by oracle/Makefile into
 // oracle/_ref/libprismint_ref.so.  Only tests/, __graft_entry__.smoke() and
 // bench.py's cpu_baseline / --impl reference leg may load it.  Nothing here
 // re-implements reference arithmetic: every entry point forwards to the

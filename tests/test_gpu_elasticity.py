@@ -163,3 +163,21 @@ def test_elasticity_inverted_element_and_errors():
             it.integrate_device(4, g, out, pb.LAPLACE)
         with pytest.raises(pb.DomainError):
             it.integrate_device(4, g, out, pb.ELASTICITY_UNIFORM, np.array([1.0, 0.5]))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_elasticity_soa_layout(p):
+    """PI_OUT_SOA ([dim^2][ld]) carries the same matrices as the canonical layout."""
+    mesh = pb.generate_box_mesh(2, 2, 1, 0.1, seed=21)
+    n = len(mesh)
+    dim = 3 * pb.shape_count(p)
+    mats = materials(n, p)
+    canon = run(p, mesh, pb.ELASTICITY, mats)
+    g = torch.from_numpy(np.ascontiguousarray(mesh.reshape(n, 18).T)).cuda()
+    c = torch.from_numpy(np.ascontiguousarray(mats.T)).cuda()
+    out = torch.full((dim * dim, n + 5), float("nan"), dtype=torch.float64, device="cuda")
+    with pb.Integrator(p, n_eq=3) as it:
+        it.integrate_device(n, g, out, pb.ELASTICITY, c, out_layout=pb.OUT_SOA, ld_out=n + 5)
+        it.check()
+    soa = out.cpu().numpy()[:, :n].T.reshape(n, dim, dim)
+    assert np.array_equal(soa, canon)
