@@ -124,11 +124,11 @@ pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base,
                        int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld,
                        double* out, int out_layout, int64_t ld_out, void* stream, pi_error_info* err);
 
-/* FP32 output variant: the same integration, K rounded
- * to float32 at the store (half the output bytes; the paper's GPU precision).
- * Stated bound: per-element relative Frobenius <= 5e-5 against the FP64
- * reference (the reference's own f32 tolerance, test_kernels.cpp:41-61);
- * measured <= 1e-7 (the arithmetic stays FP64). */
+/* FP32 variant: K in float32 (half the output bytes;
+ * the paper's GPU precision).  Scalar weak forms at p = 2 also compute in
+ * FP32 (2x the FP64 FMA rate); the other kernels compute in FP64 and round at
+ * the store.  Stated bound: per-element relative Frobenius <= 5e-5 against
+ * the FP64 reference (the reference's own f32 tolerance, test_kernels.cpp:41-61). */
 pi_status pi_integrate_f32(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
                            int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld,
                            float* out, int out_layout, int64_t ld_out, void* stream, pi_error_info* err);

@@ -29,6 +29,19 @@ namespace pib {
 constexpr int kP2NQ = 18, kP2NSH = 18, kP2KK = kP2NSH * kP2NSH;
 __constant__ double c_phi_p2[kP2NQ * 4 * kP2NSH];  // tabulate_shapes order [q][k][dof]
 __constant__ double c_pts_p2[kP2NQ * 4];           // xi1, xi2, xi3, w
+__constant__ float c_phi_p2f[kP2NQ * 4 * kP2NSH];   // the same table in FP32 (FP32 arithmetic variant)
+
+// Compute type T: double (the 1e-12 path) or float (FP32 variant, bound 5e-5).
+template <typename T>
+__device__ __forceinline__ const T* p2_phi();
+template <>
+__device__ __forceinline__ const double* p2_phi<double>() {
+  return c_phi_p2;
+}
+template <>
+__device__ __forceinline__ const float* p2_phi<float>() {
+  return c_phi_p2f;
+}
 
 constexpr int kP2Pitch = kP2KK + 1;  // odd pitch: staged elements hit distinct banks
 
@@ -79,36 +92,36 @@ __device__ __forceinline__ constexpr int p2_row(int r) {
 }
 
 // The warp's rows over all rule points.
-template <bool GENERAL, bool SYM, int W>
-__device__ __forceinline__ void p2_rows(const double* __restrict__ sM, int lane, double* acc) {
+template <typename T, bool GENERAL, bool SYM, int W>
+__device__ __forceinline__ void p2_rows(const T* __restrict__ sM, int lane, T* acc) {
   using BP = BasisPattern<2>;
   using C = P2Cfg<GENERAL, SYM>;
   constexpr int K0 = GENERAL ? 0 : 1, NR = C::NR, NM = C::NM;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
-    const double* ph = c_phi_p2 + q * 4 * kP2NSH;
-    const double* mq = sM + q * NM * 32 + lane;
+    const T* ph = p2_phi<T>() + q * 4 * kP2NSH;
+    const T* mq = sM + q * NM * 32 + lane;
     // G_l(i) = sum_k phi_k(i) M_kl, M read one row k at a time (only the
     // rows k the warp's basis functions do not annihilate)
-    double g[NR][4];
+    T g[NR][4];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-      for (int l = 0; l < 4; ++l) g[r][l] = 0.0;
+      for (int l = 0; l < 4; ++l) g[r][l] = T(0);
 #pragma unroll
     for (int k = K0; k < 4; ++k) {
       bool need = false;
 #pragma unroll
       for (int r = 0; r < NR; ++r) need = need || BP::nz(k, p2_row<NR, W>(r));
       if (!need) continue;
-      double mk[4];
+      T mk[4];
 #pragma unroll
       for (int l = K0; l < 4; ++l) mk[l] = mq[p2_mslot<GENERAL>(k, l) * 32];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const int i = p2_row<NR, W>(r);
         if (BP::nz(k, i)) {
-          const double f = ph[k * kP2NSH + i];
+          const T f = ph[k * kP2NSH + i];
 #pragma unroll
           for (int l = K0; l < 4; ++l) g[r][l] = fma(f, mk[l], g[r][l]);
         }
@@ -120,7 +133,7 @@ __device__ __forceinline__ void p2_rows(const double* __restrict__ sM, int lane,
       const int i = p2_row<NR, W>(r);
 #pragma unroll
       for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
-        double s = acc[off + j - (SYM ? i : 0)];
+        T s = acc[off + j - (SYM ? i : 0)];
 #pragma unroll
         for (int l = K0; l < 4; ++l)
           if (BP::nz(l, j)) s = fma(g[r][l], ph[l * kP2NSH + j], s);
@@ -135,24 +148,25 @@ __device__ __forceinline__ void p2_rows(const double* __restrict__ sM, int lane,
 // warp-uniform), so all 18 warps run the same instruction stream: G is
 // formed densely from the warp-uniform phi_k(i), the column loop skips the
 // structural zeros of phi_l(j) at compile time.
-__device__ __forceinline__ void p2_row_general(const double* __restrict__ sM, int lane, int i, double* acc) {
+template <typename T>
+__device__ __forceinline__ void p2_row_general(const T* __restrict__ sM, int lane, int i, T* acc) {
   using BP = BasisPattern<2>;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
-    const double* ph = c_phi_p2 + q * 4 * kP2NSH;
-    const double* mq = sM + q * 16 * 32 + lane;
-    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    const T* ph = p2_phi<T>() + q * 4 * kP2NSH;
+    const T* mq = sM + q * 16 * 32 + lane;
+    T g[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const double f = ph[k * kP2NSH + i];
-      if (f != 0.0) {  // warp-uniform: skips the M rows the basis function annihilates
+      const T f = ph[k * kP2NSH + i];
+      if (f != T(0)) {  // warp-uniform: skips the M rows the basis function annihilates
 #pragma unroll
         for (int l = 0; l < 4; ++l) g[l] = fma(f, mq[(k * 4 + l) * 32], g[l]);
       }
     }
 #pragma unroll
     for (int j = 0; j < kP2NSH; ++j) {
-      double s = acc[j];
+      T s = acc[j];
 #pragma unroll
       for (int l = 0; l < 4; ++l)
         if (BP::nz(l, j)) s = fma(g[l], ph[l * kP2NSH + j], s);
@@ -162,15 +176,15 @@ __device__ __forceinline__ void p2_row_general(const double* __restrict__ sM, in
 }
 
 // Writes the lane's accumulators as rows of its staged element matrix.
-template <bool SYM, int NR, int W>
-__device__ __forceinline__ void p2_stage(double* st, const double* acc) {
+template <bool SYM, int NR, int W, typename T>
+__device__ __forceinline__ void p2_stage(T* st, const T* acc) {
   int off = 0;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const int i = p2_row<NR, W>(r);
 #pragma unroll
     for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
-      const double v = acc[off + j - (SYM ? i : 0)];
+      const T v = acc[off + j - (SYM ? i : 0)];
       st[i * kP2NSH + j] = v;
       if (SYM && j > i) st[j * kP2NSH + i] = v;
     }
@@ -178,8 +192,8 @@ __device__ __forceinline__ void p2_stage(double* st, const double* acc) {
   }
 }
 
-template <bool SYM, int NR, int W>
-__device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, const double* acc) {
+template <bool SYM, int NR, int W, typename T>
+__device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, const T* acc) {
   int off = 0;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -210,12 +224,12 @@ __device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, 
     default: CALL(8); break; \
   }
 
-template <bool GENERAL, bool SYM>
+template <bool GENERAL, bool SYM, typename T = double>
 __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(LaunchArgs args) {
   using C = P2Cfg<GENERAL, SYM>;
   constexpr int NR = C::NR;
   extern __shared__ __align__(16) double p2_smem[];
-  double* sM = p2_smem;  // M [q][NM][32], then the output staging
+  T* sM = reinterpret_cast<T*>(p2_smem);  // M [q][NM][32], then the output staging (same byte size as FP64)
   double* sD = p2_smem + C::OFF_D;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t groups = (args.n_elem + 31) / 32;
@@ -268,21 +282,21 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
         inverted |= !(det > 0.0);
         if (GENERAL) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) sM[(q * 16 + k) * 32 + lane] = M[k];
+          for (int k = 0; k < 16; ++k) sM[(q * 16 + k) * 32 + lane] = static_cast<T>(M[k]);
         } else {
           const int src[6] = {5, 6, 7, 10, 11, 15};
 #pragma unroll
-          for (int k = 0; k < 6; ++k) sM[(q * 6 + k) * 32 + lane] = M[src[k]];
+          for (int k = 0; k < 6; ++k) sM[(q * 6 + k) * 32 + lane] = static_cast<T>(M[src[k]]);
         }
       }
       if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
     }
     __syncthreads();
-    double acc[C::NACC];
+    T acc[C::NACC];
 #pragma unroll
-    for (int i = 0; i < C::NACC; ++i) acc[i] = 0.0;
+    for (int i = 0; i < C::NACC; ++i) acc[i] = T(0);
     if constexpr (SYM) {
-#define P2_ACC(W) p2_rows<GENERAL, SYM, W>(sM, lane, acc)
+#define P2_ACC(W) p2_rows<T, GENERAL, SYM, W>(sM, lane, acc)
       P2_WARP_SWITCH(P2_ACC)
 #undef P2_ACC
     } else {
@@ -305,7 +319,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
 #pragma unroll 1
     for (int h = 0; h < 32 / C::ROUND; ++h) {
       if (lane / C::ROUND == h) {
-        double* st = sM + (lane % C::ROUND) * kP2Pitch;
+        T* st = sM + (lane % C::ROUND) * kP2Pitch;
         if constexpr (SYM) {
 #define P2_STAGE(W) p2_stage<SYM, NR, W>(st, acc)
           P2_WARP_SWITCH(P2_STAGE)

@@ -33,6 +33,8 @@ struct pi_context {
   bool tensor_ok = false;
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
+  int p2_ctas_f[3] = {0, 0, 0};  // ... and per FP32-arithmetic instantiation
+  std::vector<float> h_phi_f;    // p = 2 shape table in FP32
   int e1_ctas = 0;             // persistent grid of p1_elastic_lane_kernel
   int e2_ctas = 0;             // persistent grid of p2_elastic_warp_kernel
   int e3_ctas = 0;             // persistent grid of p3_elastic_cta_kernel
@@ -229,6 +231,16 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
     ctx->p2_ctas[0] = ctas(p2_lane_kernel<false, true>, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES);
     ctx->p2_ctas[1] = ctas(p2_lane_kernel<true, true>, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES);
     ctx->p2_ctas[2] = ctas(p2_lane_kernel<true, false>, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES);
+    cudaFuncSetAttribute(p2_lane_kernel<false, true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<false, true>::SMEM_BYTES));
+    cudaFuncSetAttribute(p2_lane_kernel<true, true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, true>::SMEM_BYTES));
+    cudaFuncSetAttribute(p2_lane_kernel<true, false, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, false>::SMEM_BYTES));
+    ctx->p2_ctas_f[0] = ctas(p2_lane_kernel<false, true, float>, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES);
+    ctx->p2_ctas_f[1] = ctas(p2_lane_kernel<true, true, float>, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES);
+    ctx->p2_ctas_f[2] = ctas(p2_lane_kernel<true, false, float>, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES);
+    ctx->h_phi_f.assign(ctx->h_phi.begin(), ctx->h_phi.end());
     ctx->p2_ok = true;
   }
   ce = cudaGetLastError();
@@ -396,13 +408,28 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
             "upload p=2 rule");
     const int64_t groups = (n_elem + 31) / 32;
     const int which = !general ? 0 : (symmetric ? 1 : 2);
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas[which]));
-    if (!general)
-      p2_lane_kernel<false, true><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
-    else if (symmetric)
-      p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
-    else
-      p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
+    if (out32) {
+      // FP32 output variant: FP32 arithmetic too (the table in FP32, M rounded
+      // after the FP64 point block); bound 5e-5
+      PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2f, ctx->h_phi_f.data(), sizeof(float) * kP2NQ * 4 * kP2NSH, 0,
+                                      cudaMemcpyHostToDevice, s),
+              "upload p=2 FP32 shape table");
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas_f[which]));
+      if (!general)
+        p2_lane_kernel<false, true, float><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
+      else if (symmetric)
+        p2_lane_kernel<true, true, float><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
+      else
+        p2_lane_kernel<true, false, float><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
+    } else {
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas[which]));
+      if (!general)
+        p2_lane_kernel<false, true><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
+      else if (symmetric)
+        p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
+      else
+        p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
+    }
   } else if (v == PI_VARIANT_DENSE && ne == 1) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     if (general) {

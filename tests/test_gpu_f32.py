@@ -1,7 +1,8 @@
-"""FP32 output variant: K rounded to float32 at the
-store.  Stated bound: per-element relative Frobenius <= 5e-5 against the
-FP64 reference -- the reference's own f32 tolerance (test_kernels.cpp:41-61);
-the arithmetic stays FP64, so the measured error is float rounding (~1e-7)."""
+"""FP32 variant: K in float32.  Stated bound: per-element
+relative Frobenius <= 5e-5 against the FP64 reference -- the reference's own
+f32 tolerance (test_kernels.cpp:41-61).  The scalar p = 2 lane kernels compute
+in FP32 (measured ~1e-6); every other kernel computes in FP64 and rounds at
+the store, so its FP32 matrices are exactly the FP64 ones rounded."""
 import numpy as np
 import pytest
 
@@ -49,9 +50,12 @@ def test_f32_output_bound(p, form):
     k64 = run(p, mesh, mode, coeff, torch.float64, n_eq)
     assert np.isfinite(k32).all()
     err = rel_frobenius(k64, k32, axis=(1, 2))
-    assert err.max() <= BOUND and err.max() <= 1e-6, err.max()
-    # the FP32 matrices are exactly the FP64 ones rounded
-    assert np.array_equal(k32, k64.astype(np.float32).astype(np.float64))
+    assert err.max() <= BOUND, err.max()
+    if p == 2 and n_eq == 1:  # FP32 arithmetic
+        assert err.max() <= 1e-5, err.max()
+    else:  # FP64 arithmetic: the FP32 matrices are exactly the FP64 ones rounded
+        assert err.max() <= 1e-6, err.max()
+        assert np.array_equal(k32, k64.astype(np.float32).astype(np.float64))
 
 
 @pytest.mark.parametrize("p", [1, 2, 4, 5])
