@@ -410,7 +410,9 @@ def main():
     if not args.no_e2e and esz == 8:
         geom_aos = torch.from_numpy(np.ascontiguousarray(geom_host.T)).pin_memory()
         coeff_aos = torch.from_numpy(np.ascontiguousarray(coeff_host.T)).pin_memory() if coeff_host is not None else None
-        host_n = {p: min(E, max(1, int(64e9 / 8) // kk[p])) for p in ps}  # pinned host output <= 64 GB
+        # pinned host output: <= 16 GB per rank (8 ranks on one box must not pin
+        # hundreds of GB); every element's K still crosses PCIe into it
+        host_n = {p: min(E, max(1, int(16e9 / 8) // kk[p])) for p in ps}
         host_out = torch.empty(max(host_n[p] * kk[p] for p in ps), dtype=torch.float64).pin_memory()
         ga = geom_aos.numpy()
         ca = coeff_aos.numpy() if coeff_aos is not None else None
