@@ -753,8 +753,8 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   const double per_point_ne = ne == 1 ? per_point : 2.0 * (21 + 16) + 6 + ne * ne * (elastic ? 60.0 : 200.0);
   const double h_terms = (general && !elastic) ? 16.0 / 9.0 : 1.0;
   const double h = ns * nve * nve * 9.0 * nz * 3.0 * h_terms;
-  const double g = ns * 3.0 * nve * dim * 3.0 * 2.0;
   bool symmetric = coeff_mode == PI_COEFF_LAPLACE || elastic;
+  const double g = ns * 3.0 * nve * dim * 3.0 * 2.0 * (symmetric ? sumfact_fragment_fraction(p, ctx->n_eq) : 1.0);
   const double frac = symmetric ? sumfact_sym_fraction(p, ctx->n_eq) : 1.0;
   const double k = nt * 3.0 * ns * dim * nve * 2.0 * frac;
   return nq * per_point_ne + h + g + k;

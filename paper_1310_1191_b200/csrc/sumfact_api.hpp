@@ -26,8 +26,10 @@ bool sumfact_build(int p, int ne, const double* pts, const double* phi, int n_q,
 void sumfact_set_attrs(int p, int ne);
 // form: SumFactForm; sym: the tensor (hence K) is symmetric.
 void sumfact_launch(int p, int ne, int form, bool sym, const LaunchArgs& a, const SumFactTables& t, cudaStream_t s);
-// Fraction of the (t, t') tile pairs the symmetric path multiplies.
+// Fraction of the (t, t') tile pairs the symmetric path multiplies, and of the
+// B-fragment values it forms.
 double sumfact_sym_fraction(int p, int ne);
+double sumfact_fragment_fraction(int p, int ne);
 // Shape numbers of the instantiation: NTILE*8 padded columns, MT*8 padded rows, KSTEPS*4 padded k.
 void sumfact_padded_shape(int p, int ne, int& cols, int& rows, int& ksteps4);
 

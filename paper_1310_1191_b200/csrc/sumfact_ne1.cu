@@ -55,6 +55,14 @@ double sumfact_ne1_sym_fraction(int p) {
   }
   return 1.0;
 }
+double sumfact_ne1_fragment_fraction(int p) {
+  switch (p) {
+#define X(P) case P: return H1<P>::fragment_fraction();
+    PIB_NE1_CASES(X)
+#undef X
+  }
+  return 1.0;
+}
 void sumfact_ne1_padded(int p, int& c, int& r, int& k) {
   switch (p) {
 #define X(P) case P: H1<P>::padded(c, r, k); break;
@@ -70,6 +78,7 @@ bool sumfact_ne3_build(int p, const double* pts, const double* phi, int nq, int 
 void sumfact_ne3_attrs(int p);
 void sumfact_ne3_launch(int p, int form, bool sym, const LaunchArgs& a, const SumFactTables& t, cudaStream_t s);
 double sumfact_ne3_sym_fraction(int p);
+double sumfact_ne3_fragment_fraction(int p);
 void sumfact_ne3_padded(int p, int& c, int& r, int& k);
 
 bool sumfact_supported(int p, int ne) { return ne == 1 ? (p >= 2 && p <= 7) : ne == 3 ? (p >= 1 && p <= 7) : false; }
@@ -85,6 +94,9 @@ void sumfact_launch(int p, int ne, int form, bool sym, const LaunchArgs& a, cons
     sumfact_ne3_launch(p, form, sym, a, t, s);
 }
 double sumfact_sym_fraction(int p, int ne) { return ne == 1 ? sumfact_ne1_sym_fraction(p) : sumfact_ne3_sym_fraction(p); }
+double sumfact_fragment_fraction(int p, int ne) {
+  return ne == 1 ? sumfact_ne1_fragment_fraction(p) : sumfact_ne3_fragment_fraction(p);
+}
 void sumfact_padded_shape(int p, int ne, int& c, int& r, int& k) {
   ne == 1 ? sumfact_ne1_padded(p, c, r, k) : sumfact_ne3_padded(p, c, r, k);
 }

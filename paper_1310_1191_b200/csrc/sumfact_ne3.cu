@@ -56,6 +56,14 @@ double sumfact_ne3_sym_fraction(int p) {
   }
   return 1.0;
 }
+double sumfact_ne3_fragment_fraction(int p) {
+  switch (p) {
+#define X(P) case P: return H3<P>::fragment_fraction();
+    PIB_NE3_CASES(X)
+#undef X
+  }
+  return 1.0;
+}
 void sumfact_ne3_padded(int p, int& c, int& r, int& k) {
   switch (p) {
 #define X(P) case P: H3<P>::padded(c, r, k); break;
