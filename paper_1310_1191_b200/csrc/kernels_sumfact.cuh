@@ -251,6 +251,9 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   // canonical order (one spare double to match the global address mod 16)
   // and stored by the TMA bulk engine.
   static constexpr bool BULK = L::TMAJOR && NAG == 1;
+  // symmetric forms: warps own (a', b') pairs a' <= b' (kernel PAIRS), when
+  // the diagonal and off-diagonal pairs split evenly over an element's warps
+  static constexpr bool PAIRS = BULK && S::NVE % WPE == 0 && (S::NVE * (S::NVE - 1) / 2) % WPE == 0;
   static constexpr int ESTRIDE = (S::NSH * S::NSH + 3) / 2 * 2;
   static constexpr int STAGE_PER_WARP = L::TMAJOR ? (L::WA * S::NT * S::NSH + 1) / 2 * 2 : 0;
   static constexpr int OFF_STAGE = (OFF_W + S::NQ + 1) / 2 * 2;
@@ -297,9 +300,9 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
   // diagonal are neither multiplied nor their B fragments formed (27 % fewer
   // MMAs, 40 % fewer fragment FMAs at p = 4); mirrors come from the staging.
   constexpr int NPAIR = C::NVE * (C::NVE + 1) / 2;
-  constexpr bool PAIRS = SYMK && C::WA == 1 && C::WPE == C::NVE && (C::NVE & 1) == 1 && C::BULK;
-  constexpr int PPW = PAIRS ? (C::NVE + 1) / 2 : 1;  // pairs per warp
-  static_assert(!PAIRS || PPW * C::MT <= C::NB, "pair accumulators reuse the t'-major array");
+  constexpr bool PAIRS = C::PAIRS && SYM;
+  constexpr int PPW = PAIRS ? NPAIR / C::WPE : 1;     // pairs per warp
+  constexpr int NDW = PAIRS ? C::NVE / C::WPE : 1;    // diagonal pairs per warp (first NDW)
   constexpr int NV = C::NV, NVE = C::NVE, NZ = C::NZ, NT = C::NT, NS = C::NS, NSH = C::NSH, NQ = C::NQ;
   constexpr int NTPS = C::NTPS, MT = C::MT, KSTEPS = C::KSTEPS, EPC = C::EPC, AG = C::AG, WA = C::WA, NB = C::NB;
   constexpr int NCHUNK = C::NCHUNK, NCOEF = C::NCOEF;
@@ -497,13 +500,14 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
   const int nblk = r_w % C::NBLK;
   const int cpos = lane >> 2;            // B-fragment column within an n-tile
   const int64_t kk_elem = static_cast<int64_t>(NSH) * NSH;
-  // PAIRS: pair 0 = (r_w, r_w); pairs 1.. = off-diagonal (a < b) number 2 r_w + pp - 1
+  // PAIRS: pairs 0..NDW-1 = diagonal (d, d), d = NDW r_w + pp; the rest are
+  // off-diagonal pairs (a < b) number (PPW - NDW) r_w + pp - NDW
   int pa[PPW], pb[PPW];
 #pragma unroll
   for (int pp = 0; pp < PPW; ++pp) {
-    pa[pp] = pb[pp] = r_w;
-    if (pp > 0) {
-      int o = (PPW - 1) * r_w + pp - 1, a = 0;
+    pa[pp] = pb[pp] = NDW * r_w + pp;
+    if (pp >= NDW) {
+      int o = (PPW - NDW) * r_w + pp - NDW, a = 0;
       while (o >= C::NVE - 1 - a) o -= C::NVE - 1 - a++;
       pa[pp] = a;
       pb[pp] = a + 1 + o;
@@ -563,13 +567,23 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) xoff[nb] = xoff0[nb] + tp_cb;
 
-    double acc[WA][MT][NB][2];
+    double acc[PAIRS ? 1 : WA][MT][PAIRS ? 1 : NB][2];
+    double accp[PPW][MT][PAIRS ? MT : 1][2];  // PAIRS: [pair][m-tile][t'-group]
+    if constexpr (PAIRS) {
 #pragma unroll
-    for (int wa = 0; wa < WA; ++wa)
+      for (int pp = 0; pp < PPW; ++pp)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb) acc[wa][mt][nb][0] = acc[wa][mt][nb][1] = 0.0;
+          for (int g = 0; g < MT; ++g) accp[pp][mt][g][0] = accp[pp][mt][g][1] = 0.0;
+    } else {
+#pragma unroll
+      for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) acc[wa][mt][nb][0] = acc[wa][mt][nb][1] = 0.0;
+    }
 
 #pragma unroll 1
     for (int chunk = 0; chunk < NCHUNK; ++chunk, ++gc) {
@@ -607,7 +621,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
-                  if (pp > 0 || g >= mt) dmma_8x8x4(acc[0][mt][pp * MT + g][0], acc[0][mt][pp * MT + g][1], afr[mt], gv);
+                  if (pp >= NDW || g >= mt) dmma_8x8x4(accp[pp][mt][g][0], accp[pp][mt][g][1], afr[mt], gv);
               }
             }
           } else {
@@ -701,15 +715,15 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           for (int mt = 0; mt < MT; ++mt) {
             const int t = mt * 8 + (lane >> 2);
 #pragma unroll
-            for (int g = (pp == 0 ? mt : 0); g < MT; ++g)
+            for (int g = (pp < NDW ? mt : 0); g < MT; ++g)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int tp = g * 8 + 2 * (lane & 3) + h;
                 if (t < NT && tp < NT) {
-                  const double v = acc[0][mt][pp * MT + g][h];
+                  const double v = accp[pp][mt][g][h];
                   const int row = t * NVE + pa[pp], col = tp * NVE + pb[pp];
                   put(row * NSH + col, v);
-                  if (pp > 0 || g > mt) put(col * NSH + row, v);  // the skipped mirror block
+                  if (pp >= NDW || g > mt) put(col * NSH + row, v);  // the skipped mirror block
                 }
               }
           }

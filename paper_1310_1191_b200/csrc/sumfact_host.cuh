@@ -115,7 +115,7 @@ struct SumFactHost {
   // whose largest t' lies below the m-tile).
   static double sym_fraction() {
     if (C::NAG != 1 || C::NCB != 1) return 1.0;
-    if (C::TMAJOR && C::WA == 1 && C::WPE == C::NVE && (C::NVE & 1) == 1 && C::BULK) {
+    if (C::PAIRS) {
       // (a', b') pairs with a' <= b' (kernels_sumfact.cuh PAIRS)
       const double mt = C::MT, nve = C::NVE;
       return (nve * mt * (mt + 1) / 2 + nve * (nve - 1) / 2 * mt * mt) / (nve * nve * mt * mt);
@@ -137,8 +137,7 @@ struct SumFactHost {
   }
   // fraction of the B-fragment values the symmetric path forms (PAIRS: a' <= b')
   static double fragment_fraction() {
-    if (C::TMAJOR && C::NAG == 1 && C::WA == 1 && C::WPE == C::NVE && (C::NVE & 1) == 1 && C::BULK)
-      return (C::NVE + 1) / (2.0 * C::NVE);
+    if (C::PAIRS) return (C::NVE + 1) / (2.0 * C::NVE);
     return 1.0;
   }
   static void padded(int& cols, int& rows, int& k4) {
