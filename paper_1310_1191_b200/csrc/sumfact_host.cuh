@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "kernels_pairs.cuh"
 #include "kernels_sumfact.cuh"
 #include "sumfact_api.hpp"
 
@@ -33,8 +34,45 @@ struct SumFactHost {
     }
     return c;
   }
+  // symmetric forms at high p: the pair-split kernel (kernels_pairs.cuh)
+  // (measured: faster for scalar forms at p >= 5; slower for n_eq = 3, whose
+  // per-chunk M blocks the pair items would rebuild per item)
+#ifndef PI_PAIRS_MINP
+#define PI_PAIRS_MINP 5
+#endif
+  static constexpr bool kPairs = NE == 1 && P >= PI_PAIRS_MINP;
+  template <int FORM>
+  static void attr_pairs() {
+    if constexpr (kPairs)
+      cudaFuncSetAttribute(sumfact_pairs_kernel<P, NE, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(PairsConfig<P, NE>::SMEM_BYTES));
+  }
+  template <int FORM>
+  static bool go_pairs(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
+    if constexpr (kPairs) {
+      using PC = PairsConfig<P, NE>;
+      static int c = 0;
+      if (c == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_pairs_kernel<P, NE, FORM>, PC::NTHREADS,
+                                                      PC::SMEM_BYTES);
+        c = std::max(1, sms * std::max(1, per_sm));
+      }
+      const int64_t items = a.n_elem * PC::NITEM;
+      const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, c)));
+      sumfact_pairs_kernel<P, NE, FORM><<<grid, PC::NTHREADS, PC::SMEM_BYTES, s>>>(a, t);
+      return true;
+    }
+    return false;
+  }
   template <int FORM, bool SYM>
   static void go(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
+#ifndef PI_NO_PAIRS
+    if constexpr (SYM)
+      if (go_pairs<FORM>(a, t, s)) return;
+#endif
     const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NITEM;
     const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<FORM, SYM>())));
     sumfact_kernel<P, NE, FORM, SYM><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);

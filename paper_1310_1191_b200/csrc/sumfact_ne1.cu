@@ -18,6 +18,8 @@ void launch1(int form, bool sym, const LaunchArgs& a, const SumFactTables& t, cu
 template <int P>
 void attrs1() {
   H1<P>::template attr<kFormLaplace, true>();
+  H1<P>::template attr_pairs<kFormLaplace>();
+  H1<P>::template attr_pairs<kFormGeneral>();
   H1<P>::template attr<kFormGeneral, true>();
   H1<P>::template attr<kFormGeneral, false>();
 }

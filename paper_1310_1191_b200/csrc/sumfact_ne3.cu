@@ -19,6 +19,8 @@ void launch3(int form, bool sym, const LaunchArgs& a, const SumFactTables& t, cu
 template <int P>
 void attrs3() {
   H3<P>::template attr<kFormElasticity, true>();
+  H3<P>::template attr_pairs<kFormElasticity>();
+  H3<P>::template attr_pairs<kFormGeneral>();
   H3<P>::template attr<kFormGeneral, true>();
   H3<P>::template attr<kFormGeneral, false>();
 }
