@@ -1,4 +1,6 @@
-// Symmetric sum factorisation over (a', b') PAIRS across CTAs (p >= 5).
+// Symmetric sum factorisation over (a', b') PAIRS across CTAs (scalar forms,
+// p >= 5; at p <= 4 a CTA holds whole elements and kernels_sumfact.cuh pairs
+// within the CTA; for n_eq = 3 the row split measured faster).
 //
 // For a symmetric coefficient tensor K is symmetric:
 //     K[(t,a'),(t',b')] = K[(t',b'),(t,a')],
