@@ -41,6 +41,10 @@ def parse_launches(path):
 def kernel_key(name):
     """Kernel name -> (p, weak form): sumfact_kernel<P, NE, FORM, SYM>,
     p1_thread_kernel<GENERAL>, p2_lane_kernel<GENERAL, SYM>."""
+    n_eq3 = {"p1_elastic_lane_kernel": 1, "p2_elastic_warp_kernel": 2, "p3_elastic_cta_kernel": 3}
+    for k, p in n_eq3.items():
+        if k in name:
+            return p, "elasticity"
     inside = name.split("<")[1].rstrip(">").replace(" ", "").replace("(int)", "").replace("(bool)", "").split(",")
     general = lambda v: v in ("1", "true")  # noqa: E731
     if "p1_thread" in name:
