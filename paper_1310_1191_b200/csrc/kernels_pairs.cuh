@@ -120,8 +120,10 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
   const double* Pv = sY;            // P_a(z)  [NZ][NV]
   const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]
 
-  const int64_t n_items = args.n_elem * C::NITEM;
-  const int64_t my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // Element-major: a CTA takes elements blockIdx.x + k * gridDim.x and walks
+  // all NITEM pair groups of each, so M is built once per element.
+  const int64_t my_elems = blockIdx.x < args.n_elem ? (args.n_elem - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_items = my_elems * C::NITEM;
   const int64_t total_chunks = my_items * NCHUNK;
 
   if (warp >= C::NCW) {
@@ -177,9 +179,8 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
       named_sync(C::BAR_PROD, C::NPT);
     };
     for (int64_t it = 0; it < my_items; ++it) {
-      const int64_t w = blockIdx.x + it * gridDim.x;
-      const int64_t e = w / C::NITEM;
-      const int p0 = static_cast<int>(w % C::NITEM) * C::PPI;  // first pair of the item
+      const int64_t e = blockIdx.x + (it / C::NITEM) * gridDim.x;
+      const int p0 = static_cast<int>(it % C::NITEM) * C::PPI;  // first pair of the item
       if (C::MALL) {
         if (e != loaded) {  // a new element: M for all its points into the other buffer
           mb = loaded < 0 ? 0 : mb ^ 1;
@@ -244,9 +245,8 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
   }
   int64_t gc = 0;
   for (int64_t it = 0; it < my_items; ++it) {
-    const int64_t w = blockIdx.x + it * gridDim.x;
-    const int64_t e = w / C::NITEM;
-    const int p0 = static_cast<int>(w % C::NITEM) * C::PPI + warp * PPW;
+    const int64_t e = blockIdx.x + (it / C::NITEM) * gridDim.x;
+    const int p0 = static_cast<int>(it % C::NITEM) * C::PPI + warp * PPW;
     int pa[PPW], pb[PPW];
     bool live[PPW];
 #pragma unroll

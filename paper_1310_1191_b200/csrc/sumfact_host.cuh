@@ -60,8 +60,7 @@ struct SumFactHost {
                                                       PC::SMEM_BYTES);
         c = std::max(1, sms * std::max(1, per_sm));
       }
-      const int64_t items = a.n_elem * PC::NITEM;
-      const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, c)));
+      const dim3 grid(static_cast<unsigned>(std::min<int64_t>(a.n_elem, c)));  // element-major CTAs
       sumfact_pairs_kernel<P, NE, FORM><<<grid, PC::NTHREADS, PC::SMEM_BYTES, s>>>(a, t);
       return true;
     }
