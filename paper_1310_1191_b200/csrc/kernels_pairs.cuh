@@ -74,12 +74,31 @@ struct PairsConfig {
   static constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + NBUF, BAR_PROD = 1 + 2 * NBUF;
 };
 
-// pair index -> (a', b') with a' <= b', row-major over the upper triangle
+// pair index -> (a', b') with a' <= b'.  Pairs are ordered by 4 x 4 blocks of
+// the (a', b') triangle (blocks row-major, pairs row-major inside a block), so
+// consecutive items complete whole 32-byte sectors of K -- 4 consecutive b'
+// of a row, and in the mirrored rows 4 consecutive a' -- while they are in L2.
 __device__ __forceinline__ void pair_decode(int k, int nve, int& a, int& b) {
-  int i = 0;
-  while (k >= nve - i) k -= nve - i++;
-  a = i;
-  b = i + k;
+  const int nb = (nve + 3) / 4;
+  for (int bi = 0; bi < nb; ++bi)
+    for (int bj = bi; bj < nb; ++bj) {
+      const int a0 = 4 * bi, a1 = min(nve, a0 + 4), b0 = 4 * bj, b1 = min(nve, b0 + 4);
+      const int cnt = bi == bj ? (a1 - a0) * (a1 - a0 + 1) / 2 : (a1 - a0) * (b1 - b0);
+      if (k < cnt) {
+        if (bi == bj) {  // upper triangle of a diagonal block
+          int i = 0;
+          while (k >= (a1 - a0) - i) k -= (a1 - a0) - i++;
+          a = a0 + i;
+          b = a0 + i + k;
+        } else {
+          a = a0 + k / (b1 - b0);
+          b = b0 + k % (b1 - b0);
+        }
+        return;
+      }
+      k -= cnt;
+    }
+  a = b = 0;
 }
 
 template <int P, int NE, int FORM>
