@@ -158,6 +158,19 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
     float2* dst = reinterpret_cast<float2*>(args.out32 + first * KK);
     for (int i = tid; i < total2; i += kP1Threads) dst[i] = make_float2(static_cast<float>(so2[i].x), static_cast<float>(so2[i].y));
   } else {
+#ifndef PI_P1_NO_BULK
+    // the staging is the tile's exact global image: one TMA bulk store (16-byte
+    // aligned when the output base is; 288 B per element)
+    if ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0) {
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        bulk_store(args.out + first * KK, sOut, static_cast<unsigned>(n_here) * KK * 8u);
+        bulk_commit();
+        bulk_wait_read();  // the CTA's shared memory must outlive the copy
+      }
+      return;
+    }
+#endif
     double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
     for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
   }
