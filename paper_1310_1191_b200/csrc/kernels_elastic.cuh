@@ -28,7 +28,7 @@ __constant__ double c_phi_e1[kE1NQ * 4 * kE1NSH];  // tabulate_shapes order [q][
 __constant__ double c_pts_e1[kE1NQ * 4];           // xi1, xi2, xi3, w
 
 constexpr int kE1Warps = 3;
-constexpr int kE1Pitch = kE1KK + 1;  // odd pitch: staged elements hit distinct banks
+constexpr int kE1Pitch = kE1KK + 2;  // 16-byte multiple: staged elements leave by TMA bulk stores
 #ifndef PI_E1_ROUND
 #define PI_E1_ROUND 16
 #endif
@@ -127,10 +127,12 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
   double* sMat = e1_smem + E1Smem::OFF_MAT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t groups = (args.n_elem + 31) / 32;
+  const bool bulk = !args.out32 && args.out_layout == PI_OUT_CANONICAL && (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
   for (int64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
     const int64_t e = grp * 32 + lane;
     const bool live = e < args.n_elem;
     const int64_t ec = live ? e : args.n_elem - 1;
+    if (bulk && threadIdx.x < kE1Round) bulk_wait_read();  // last group's stores no longer read sG
     if (warp == 0) {
       double x[18], d[21];
 #pragma unroll
@@ -196,16 +198,29 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
     }
 #pragma unroll 1
     for (int h = 0; h < 32 / kE1Round; ++h) {
+      if (bulk && h > 0) {  // the previous round's bulk stores have read the staging
+        if (threadIdx.x < kE1Round) bulk_wait_read();
+        __syncthreads();
+      }
       if (lane / kE1Round == h) {
         double* st = sG + (lane % kE1Round) * kE1Pitch;
 #define E1_STAGE(W) e1_store<W>(st, 1, acc)
         E1_WARP_SWITCH(E1_STAGE)
 #undef E1_STAGE
       }
-      __syncthreads();
       const int64_t first = grp * 32 + kE1Round * h;
       const int64_t left = args.n_elem - first;
       const int n_here = left <= 0 ? 0 : (left < kE1Round ? static_cast<int>(left) : kE1Round);
+      if (bulk) {  // one TMA bulk store per staged element (2592 B)
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x < n_here) {
+          bulk_store(args.out + (first + threadIdx.x) * kE1KK, sG + threadIdx.x * kE1Pitch, kE1KK * 8u);
+          bulk_commit();
+        }
+        continue;
+      }
+      __syncthreads();
       for (int r = threadIdx.x; r < n_here * kE1KK; r += 32 * kE1Warps) {
         const int el = r / kE1KK, c = r - el * kE1KK;
         store_out(args, first * kE1KK + r, sG[el * kE1Pitch + c]);
@@ -213,6 +228,7 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
       __syncthreads();
     }
   }
+  if (threadIdx.x < kE1Round) bulk_wait_all();
 }
 #undef E1_WARP_SWITCH
 
