@@ -361,8 +361,16 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
       for (int r = lane; r < kE2KK; r += 32) store_out(args, static_cast<int64_t>(r) * args.ld_out + e, sw[r]);
     } else if (args.out32) {
       for (int r = lane; r < kE2KK; r += 32) args.out32[e * kE2KK + r] = static_cast<float>(sw[r]);
+    } else if ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0) {
+      // 2916 doubles per element, 16-byte aligned: one TMA bulk store
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store(args.out + e * kE2KK, sw, kE2KK * 8u);
+        bulk_commit();
+        bulk_wait_read();  // the next element's gradients overwrite the staging
+      }
     } else {
-      // 2916 doubles per element: every element starts 16-byte aligned
       double2* dst = reinterpret_cast<double2*>(args.out + e * kE2KK);
       const double2* src = reinterpret_cast<const double2*>(sw);
       for (int r = lane; r < kE2KK / 2; r += 32) dst[r] = src[r];
