@@ -250,10 +250,10 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   // t'-major with whole elements in the CTA: element matrices staged in
   // canonical order (one spare double to match the global address mod 16)
   // and stored by the TMA bulk engine.
-  static constexpr bool BULK = L::TMAJOR && NAG == 1;
+  static constexpr bool BULK = NAG == 1 && L::NCB == 1;  // whole elements per CTA: staged, TMA bulk stores
   // symmetric forms: warps own (a', b') pairs a' <= b' (kernel PAIRS), when
   // the diagonal and off-diagonal pairs split evenly over an element's warps
-  static constexpr bool PAIRS = BULK && S::NVE % WPE == 0 && (S::NVE * (S::NVE - 1) / 2) % WPE == 0;
+  static constexpr bool PAIRS = L::TMAJOR && BULK && S::NVE % WPE == 0 && (S::NVE * (S::NVE - 1) / 2) % WPE == 0;
   static constexpr int ESTRIDE = (S::NSH * S::NSH + 3) / 2 * 2;
   static constexpr int STAGE_PER_WARP = L::TMAJOR ? (L::WA * S::NT * S::NSH + 1) / 2 * 2 : 0;
   static constexpr int OFF_STAGE = (OFF_W + S::NQ + 1) / 2 * 2;
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
                 }
               }
           }
-      } else
+      } else if constexpr (C::TMAJOR) {
 #pragma unroll
       for (int wa = 0; wa < WA; ++wa)
 #pragma unroll
@@ -748,6 +748,34 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
                 }
               }
         }
+      } else {
+        // natural order, whole elements in the CTA (NAG == 1, NCB == 1)
+#pragma unroll
+        for (int wa = 0; wa < WA; ++wa)
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int t = mt * 8 + (lane >> 2);
+            const int row = t * NVE + al0 + wa;
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+              if (SYMN && !((need[nb] >> mt) & 1u)) continue;  // filled by the transposed tile's mirror
+              if (t >= NT) continue;
+              const int j = ntl0[nb] * 8 + 2 * (lane & 3);
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int jj = j + h;
+                if (jj >= NSH) continue;
+                const double v = acc[wa][mt][nb][h];
+                put(row * NSH + jj, v);
+                if (SYMN) {
+                  const int mt2 = (jj / NVE) >> 3;
+                  const int tmax2 = min(NT - 1, ((row >> 3) * 8 + 7) / NVE);
+                  if (tmax2 < 8 * mt2) put(jj * NSH + row, v);
+                }
+              }
+            }
+          }
+      }
       fence_proxy_async_smem();
       named_sync(kBarCons, 32 * C::NCW);
       if (bulk) {
