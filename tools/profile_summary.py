@@ -1,7 +1,7 @@
 """Turn a gpurun sweep (ncu launch list CSV) + one full ncu capture into a
 committed summary under profiles/.
 
-  python tools/profile_summary.py <tag> [--full gpurun_out/prof_<tag>_pN.ncu-rep]
+  python tools/profile_summary.py <tag> [--full gpurun_out/prof_<tag>_pN.ncu-rep ...]
 
 Writes profiles/<tag>_launches.csv (copy), profiles/<tag>.md and updates
 profiles/traffic.json (DRAM bytes per launch per (p, coeff), read by bench.py).
@@ -95,7 +95,7 @@ def full_counters(rep):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("tag")
-    ap.add_argument("--full", default=None)
+    ap.add_argument("--full", action="append", default=[])
     a = ap.parse_args()
     src = ROOT / "gpurun_out" / f"sweep_{a.tag}.csv"
     prof = ROOT / "profiles"
@@ -126,9 +126,9 @@ def main():
                      f"{n/t/bound:.2f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {8*dims(p, form)**2*n/1e6:.1f} |")
         traffic[f"p{p}_{form}"] = (rd + wr) / n  # DRAM bytes per element (per launch / elements)
     json.dump(traffic, open(tf, "w"), indent=1)
-    if a.full:
-        c = full_counters(a.full)
-        lines += ["", f"## Full capture `{Path(a.full).name}`", "", "| counter | value |", "|---|---|"]
+    for full in a.full:
+        c = full_counters(full)
+        lines += ["", f"## Full capture `{Path(full).name}`", "", "| counter | value |", "|---|---|"]
         lines += [f"| {k} | {v} |" for k, v in c.items()]
     (prof / f"{a.tag}.md").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
