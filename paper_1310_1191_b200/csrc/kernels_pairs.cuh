@@ -136,8 +136,7 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
     bulk_load(sW, tab.w, BW, &s_tables);
   }
   mbar_wait(&s_tables, 0);
-  const double* Pv = sY;            // P_a(z)  [NZ][NV]
-  const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]
+  const double2* PD = reinterpret_cast<const double2*>(sY);  // (P_a(z), P'_a(z)) [NZ][NV]
 
   // Element-major: a CTA takes elements blockIdx.x + k * gridDim.x and walks
   // all NITEM pair groups of each, so M is built once per element.
@@ -227,14 +226,16 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
 #pragma unroll
             for (int z = 0; z < NZ; ++z) {
               auto M = [Mp, z](int k) { return Mp[k * C::MPITCH + z]; };
-              const double pa = Pv[z * NV + a], da = Pd[z * NV + a];
+              const double2 yab = PD[z * NV + a];
+              const double pa = yab.x, da = yab.y;
               const double wr = x < 2 ? pa : da;
               const double w0 = (GENERAL && x == 2) ? pa : 0.0;
               const double L0 = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
               const double L1 = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
               const double L2 = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
               const double L3 = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
-              const double pb = Pv[z * NV + b], db = Pd[z * NV + b];
+              const double2 ybb = PD[z * NV + b];
+              const double pb = ybb.x, db = ybb.y;
               h0 = fma(L1, pb, h0);
               h1 = fma(L2, pb, h1);
               h2 = GENERAL ? fma(L0, pb, fma(L3, db, h2)) : fma(L3, db, h2);

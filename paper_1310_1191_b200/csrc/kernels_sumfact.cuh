@@ -212,6 +212,33 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
       }
     return worst;
   }
+  // t'-major: the producers' stores are the only H conflicts, so count the
+  // wavefronts per warp of both the 16-byte (y = 0, 1) and the 8-byte (y = 2)
+  // stores.
+  static constexpr int pwavefronts(int hb, int hs) {
+    constexpr int items = L::EPC * L::AG * 4 * 3 * L::BSPLIT;
+    int total = 0;
+    for (int w0 = 0; w0 < items; w0 += 32)
+      for (int bb = 0; bb < BPER; ++bb)
+        for (int wide = 0; wide < 2; ++wide) {
+          const int width = wide ? 8 : 16;  // lanes per wavefront
+          for (int q0 = w0; q0 < w0 + 32 && q0 < items; q0 += width) {
+            int cnt[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, worst = 0;
+            for (int i = q0; i < q0 + width && i < items; ++i) {
+              const int bg = i % L::BSPLIT, x = (i / L::BSPLIT) % 3, sl = (i / (3 * L::BSPLIT)) % 4;
+              const int alg = i / (12 * L::BSPLIT);  // (el, al)
+              const int bp = bg * BPER + bb;
+              if (bp >= S::NVE) continue;
+              const int off = alg * 4 * hs + sl * hs + bp * hb + x * 4;
+              const int k = wide ? (off / 2) % 8 : (off + 2) % 16;
+              ++cnt[k];
+              worst = worst > cnt[k] ? worst : cnt[k];
+            }
+            total += worst;
+          }
+        }
+    return total;
+  }
   static constexpr int hpick() {  // returns hb * 1024 + hs
     int best = 1 << 30, pick = 12 * 1024 + S::NVE * 12;
     for (int hb = 12; hb <= 18; hb += 2)
@@ -219,7 +246,8 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
         const int hs = S::NVE * hb + pad;
         // t'-major consumers read H warp-uniformly in b': only the stores matter there
         const int cons = L::TMAJOR ? 1 : hconflicts(hb, hs);
-        const int score = cons * 10000000 + pconflicts(hb, hs) * 10000 + hs;  // then least memory
+        const int prod = L::TMAJOR ? pwavefronts(hb, hs) : pconflicts(hb, hs);
+        const int score = cons * 10000000 + prod * 10000 + hs;  // then least memory
         if (score < best) best = score, pick = hb * 1024 + hs;
       }
     return pick;
@@ -243,7 +271,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
   static constexpr int OFF_GEOM = OFF_M + (MALL ? 2 : 1) * M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + (L::EPC * 21 + 1) / 2 * 2;
-  static constexpr int OFF_LINE = OFF_C + L::EPC * NCOEF;  // P [NV][NZ], P' [NV][NZ], xi3 [NZ]
+  static constexpr int OFF_LINE = OFF_C + L::EPC * NCOEF;  // (P, P') [NZ][NV] pairs, xi3 [NZ]
   static constexpr int OFF_TRI = OFF_LINE + (2 * S::NV * S::NZ + S::NZ + 1) / 2 * 2;
   static constexpr int OFF_W = OFF_TRI + 2 * S::NS;
   // t'-major epilogue: each consumer warp stages its WA*NT K rows
@@ -267,7 +295,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
 struct SumFactTables {
   const double* xfrag;   // X in A-fragment order [MT][KSTEPS][32]
   const double* xplain;  // X as [NSP][3][NTPS] (zero padded)
-  const double* yline;   // P [NZ][NV], P' [NZ][NV], xi3 [NZ]
+  const double* yline;   // (P, P') [NZ][NV] pairs, xi3 [NZ]
   const double* tri;     // xi1 [NS], xi2 [NS]
   const double* w;       // [NQ] rule weights (reference order)
 };
@@ -336,8 +364,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
   }
   mbar_wait(&s_tables, 0);
 
-  const double* Pv = sY;            // P_a(z)  [NZ][NV]
-  const double* Pd = sY + NV * NZ;  // P'_a(z) [NZ][NV]
+  const double2* PD = reinterpret_cast<const double2*>(sY);  // (P_a(z), P'_a(z)) [NZ][NV]
 
   // Work items: (element group, a'-group, column block); this CTA takes
   // items blockIdx.x + k*gridDim.x.
@@ -446,22 +473,33 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const double* Mz = Mp + z;
-            const double pa = Pv[z * NV + a], da = Pd[z * NV + a];
+            const double2 yab = PD[z * NV + a];
+            const double pa = yab.x, da = yab.y;
             // left factor L_l = sum_{k in x} Y_k(a) M_kl (row kx weighted by P or P',
-            // plus row 0 weighted by P for x = 2 in the general case)
+            // plus row 0 weighted by P for x = 2 in the general case); with one
+            // equation it does not depend on b', so it is formed once per z
             const double wr = x < 2 ? pa : da;
             const double w0 = (GENERAL && x == 2) ? pa : 0.0;
+            auto left = [&](int je, double (&L)[4]) {
+              auto M = [Mz, ie, je](int k) { return Mz[((ie * NE + je) * 16 + k) * C::MPITCH]; };
+              L[0] = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
+              L[1] = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
+              L[2] = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
+              L[3] = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
+            };
+            double L1e[4];
+            if (NE == 1) left(0, L1e);
 #pragma unroll
             for (int bb = 0; bb < C::BPER; ++bb) {
               const int bp = bg * C::BPER + bb;      // b' = b*NE + je
               if (bp < NVE) {
                 const int b = bp / NE, je = bp % NE;
-                auto M = [Mz, ie, je](int k) { return Mz[((ie * NE + je) * 16 + k) * C::MPITCH]; };
-                const double L0 = GENERAL ? wr * M(kx * 4 + 0) + w0 * M(0) : 0.0;
-                const double L1 = wr * M(kx * 4 + 1) + (GENERAL ? w0 * M(1) : 0.0);
-                const double L2 = wr * M(kx * 4 + 2) + (GENERAL ? w0 * M(2) : 0.0);
-                const double L3 = wr * M(kx * 4 + 3) + (GENERAL ? w0 * M(3) : 0.0);
-                const double pb = Pv[z * NV + b], db = Pd[z * NV + b];
+                double Lb[4];
+                if (NE != 1) left(je, Lb);
+                const double L0 = NE == 1 ? L1e[0] : Lb[0], L1 = NE == 1 ? L1e[1] : Lb[1];
+                const double L2 = NE == 1 ? L1e[2] : Lb[2], L3 = NE == 1 ? L1e[3] : Lb[3];
+                const double2 ybb = PD[z * NV + b];
+                const double pb = ybb.x, db = ybb.y;
                 h[bb][0] = fma(L1, pb, h[bb][0]);
                 h[bb][1] = fma(L2, pb, h[bb][1]);
                 h[bb][2] = GENERAL ? fma(L0, pb, fma(L3, db, h[bb][2])) : fma(L3, db, h[bb][2]);

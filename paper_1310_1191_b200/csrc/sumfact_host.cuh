@@ -95,13 +95,13 @@ struct SumFactHost {
       out.tri[s] = pts[3 * s];
       out.tri[NS + s] = pts[3 * s + 1];
     }
-    // Y: P_a(z) = phi_0((t=0,a), (s=0,z)), P'_a(z) = phi_3((0,a),(0,z)) since m_0 = 1.
+    // Y: [NZ][NV] pairs (P_a(z), P'_a(z)), P_a(z) = phi_0((t=0,a), (s=0,z)), P'_a(z) = phi_3((0,a),(0,z)) since m_0 = 1.
     auto& yl = out.yline;
     yl.assign(2 * NV * NZ + NZ, 0.0);
     for (int a = 0; a < NV; ++a)
       for (int z = 0; z < NZ; ++z) {
-        yl[z * NV + a] = PHI(z * NS, 0, a);
-        yl[NV * NZ + z * NV + a] = PHI(z * NS, 3, a);
+        yl[2 * (z * NV + a)] = PHI(z * NS, 0, a);      // (P, P') interleaved: one 16-byte load
+        yl[2 * (z * NV + a) + 1] = PHI(z * NS, 3, a);
       }
     for (int z = 0; z < NZ; ++z) yl[2 * NV * NZ + z] = pts[3 * z * NS + 2];
     yl.resize((yl.size() + 1) / 2 * 2, 0.0);  // 16-byte multiple for the TMA bulk copy
@@ -120,7 +120,7 @@ struct SumFactHost {
         for (int t = 0; t < NT; ++t)
           for (int a = 0; a < NV; ++a) {
             const int q = z * NS + s, dof = t * NV + a;
-            const double Pz = yl[z * NV + a], D = yl[NV * NZ + z * NV + a];
+            const double Pz = yl[2 * (z * NV + a)], D = yl[2 * (z * NV + a) + 1];
             const double m = X[(2 * NT + t) * NS + s];
             const double ref[4] = {m * Pz, X[(0 * NT + t) * NS + s] * Pz, X[(1 * NT + t) * NS + s] * Pz, m * D};
             for (int k = 0; k < 4; ++k) {
