@@ -175,25 +175,34 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   // HB and HS are padded so that the natural-order consumers' 16-byte H loads
   // (a quarter warp = 2 consecutive b' x 4 (s, x) pairs) hit distinct bank
   // groups: chosen at compile time by counting conflicts (hconflicts).
+  // Returns the wavefronts of one warp's 16-byte (y = 0, 1; quarter warps)
+  // plus 8-byte (y = 2; half warps) H loads, summed over k-steps and n-tiles.
   static constexpr int hconflicts(int hb, int hs) {
-    int worst = 0;
+    int total = 0;
     for (int ks = 0; ks < 3; ++ks)
       for (int nb = 0; nb < (NTILE < 8 ? NTILE : 8); ++nb)
-        for (int q = 0; q < 4; ++q) {
-          int offs[8] = {0, 0, 0, 0, 0, 0, 0, 0}, n = 0;
-          for (int l = 0; l < 8; ++l) {
-            const int lane = 8 * q + l, kk = 4 * ks + (lane & 3);
-            const int b = (nb * 8 + (lane >> 2)) % S::NVE;
-            const int off = (kk / 3) * hs + b * hb + (kk % 3) * 4;
-            bool seen = false;
-            for (int i = 0; i < n; ++i) seen = seen || offs[i] == off;
-            if (!seen) offs[n++] = off;
+        for (int wide = 0; wide < 2; ++wide) {
+          const int width = wide ? 8 : 16;
+          for (int q = 0; q < 32; q += width) {
+            int offs[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, n = 0;
+            for (int l = 0; l < width; ++l) {
+              const int lane = q + l, kk = 4 * ks + (lane & 3);
+              const int b = (nb * 8 + (lane >> 2)) % S::NVE;
+              const int off = (kk / 3) * hs + b * hb + (kk % 3) * 4 + (wide ? 0 : 2);
+              bool seen = false;
+              for (int i = 0; i < n; ++i) seen = seen || offs[i] == off;
+              if (!seen) offs[n++] = off;
+            }
+            int cnt[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, worst = 0;
+            for (int i = 0; i < n; ++i) {
+              const int k = wide ? (offs[i] / 2) % 8 : offs[i] % 16;
+              ++cnt[k];
+              worst = worst > cnt[k] ? worst : cnt[k];
+            }
+            total += worst;
           }
-          int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          for (int i = 0; i < n; ++i) ++cnt[(offs[i] / 2) % 8];
-          for (int g = 0; g < 8; ++g) worst = worst > cnt[g] ? worst : cnt[g];
         }
-    return worst;
+    return total;
   }
   // producers' 16-byte H stores: quarter warps of consecutive items (b'-group, x, s, ...)
   static constexpr int pconflicts(int hb, int hs) {
@@ -240,14 +249,15 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
     return total;
   }
   static constexpr int hpick() {  // returns hb * 1024 + hs
-    int best = 1 << 30, pick = 12 * 1024 + S::NVE * 12;
-    for (int hb = 12; hb <= 18; hb += 2)
+    long long best = 1LL << 62;
+    int pick = 12 * 1024 + S::NVE * 12;
+    for (int hb = 12; hb <= 24; hb += 2)
       for (int pad = 0; pad < 16; pad += 2) {
         const int hs = S::NVE * hb + pad;
         // t'-major consumers read H warp-uniformly in b': only the stores matter there
         const int cons = L::TMAJOR ? 1 : hconflicts(hb, hs);
         const int prod = L::TMAJOR ? pwavefronts(hb, hs) : pconflicts(hb, hs);
-        const int score = cons * 10000000 + prod * 10000 + hs;  // then least memory
+        const long long score = cons * 1000000000LL + prod * 10000LL + hs;  // then least memory
         if (score < best) best = score, pick = hb * 1024 + hs;
       }
     return pick;
