@@ -171,31 +171,30 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int RC = R < L::NB ? R : L::NB;     // distinct b' values a lane touches
   static_assert(S::NVE % L::AG == 0 && L::AG % L::WA == 0, "bad a-grouping");
   static_assert(NTILE % (L::NB * L::NCB) == 0, "n-tiles must split evenly");
-  // H for one chunk: [EPC][AG][4 s (stride HS)][NVE b' (stride HB)][3 x][4 y (padded)].
-  // HB and HS are padded so that the natural-order consumers' 16-byte H loads
-  // (a quarter warp = 2 consecutive b' x 4 (s, x) pairs) hit distinct bank
-  // groups: chosen at compile time by counting conflicts (hconflicts).
-  // Returns the wavefronts of one warp's 16-byte (y = 0, 1; quarter warps)
-  // plus 8-byte (y = 2; half warps) H loads, summed over k-steps and n-tiles.
-  static constexpr int hconflicts(int hb, int hs) {
+  // H for one chunk, two planes per ring buffer, indexed by one offset
+  //   o = ((el*AG + a')*4 + s)*HS2 + b'*HB2 + x:
+  //     y = 0, 1 at H[2o], H[2o + 1]   (16-byte loads / stores)
+  //     y = 2    at H[H2OFF + o]        (8-byte loads / stores)
+  // The strides are padded at compile time by counting the shared-memory
+  // wavefronts of one warp's consumer loads and producer stores in both
+  // planes (hwave): the 16-byte plane is bank-conflict free when the o of a
+  // quarter warp differ mod 8, the 8-byte plane when those of a half warp
+  // differ mod 16.
+  static constexpr int hwave_cons(int hb2, int hs2) {
     int total = 0;
+    constexpr int NBM = L::TMAJOR ? (S::NVE < 8 ? S::NVE : 8) : (NTILE < 8 ? NTILE : 8);
     for (int ks = 0; ks < 3; ++ks)
-      for (int nb = 0; nb < (NTILE < 8 ? NTILE : 8); ++nb)
-        for (int wide = 0; wide < 2; ++wide) {
-          const int width = wide ? 8 : 16;
+      for (int nb = 0; nb < NBM; ++nb)
+        for (int plane = 0; plane < 2; ++plane) {
+          const int width = plane == 0 ? 8 : 16, mod = plane == 0 ? 8 : 16;
           for (int q = 0; q < 32; q += width) {
-            int offs[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, n = 0;
-            for (int l = 0; l < width; ++l) {
-              const int lane = q + l, kk = 4 * ks + (lane & 3);
-              const int b = (nb * 8 + (lane >> 2)) % S::NVE;
-              const int off = (kk / 3) * hs + b * hb + (kk % 3) * 4 + (wide ? 0 : 2);
-              bool seen = false;
-              for (int i = 0; i < n; ++i) seen = seen || offs[i] == off;
-              if (!seen) offs[n++] = off;
-            }
             int cnt[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, worst = 0;
-            for (int i = 0; i < n; ++i) {
-              const int k = wide ? (offs[i] / 2) % 8 : offs[i] % 16;
+            // natural order: b' = (8 nt + lane/4) mod NVE, every lane distinct;
+            // t'-major: one b' per warp, lanes 4..7 of a group repeat lanes 0..3
+            for (int l = 0; l < (L::TMAJOR ? 4 : width); ++l) {
+              const int lane = q + l, kk = 4 * ks + (lane & 3);
+              const int b = L::TMAJOR ? nb : (nb * 8 + (lane >> 2)) % S::NVE;
+              const int k = ((kk / 3) * hs2 + b * hb2 + (kk % 3)) % mod;
               ++cnt[k];
               worst = worst > cnt[k] ? worst : cnt[k];
             }
@@ -204,42 +203,22 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
         }
     return total;
   }
-  // producers' 16-byte H stores: quarter warps of consecutive items (b'-group, x, s, ...)
-  static constexpr int pconflicts(int hb, int hs) {
-    int worst = 0;
-    constexpr int items = L::EPC * L::AG * 4 * 3 * L::BSPLIT;
-    for (int q0 = 0; q0 < items; q0 += 8)
-      for (int bb = 0; bb < BPER; ++bb) {
-        int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = q0; i < q0 + 8 && i < items; ++i) {
-          const int bg = i % L::BSPLIT, x = (i / L::BSPLIT) % 3, sl = (i / (3 * L::BSPLIT)) % 4;
-          const int alg = i / (12 * L::BSPLIT);  // (el, al)
-          const int off = alg * 4 * hs + sl * hs + (bg * BPER + bb) * hb + x * 4;
-          ++cnt[(off / 2) % 8];
-        }
-        for (int g = 0; g < 8; ++g) worst = worst > cnt[g] ? worst : cnt[g];
-      }
-    return worst;
-  }
-  // t'-major: the producers' stores are the only H conflicts, so count the
-  // wavefronts per warp of both the 16-byte (y = 0, 1) and the 8-byte (y = 2)
-  // stores.
-  static constexpr int pwavefronts(int hb, int hs) {
+  // producers: consecutive items (b'-group, x, s, (el, a')) per lane, b' looped
+  static constexpr int hwave_prod(int hb2, int hs2) {
     constexpr int items = L::EPC * L::AG * 4 * 3 * L::BSPLIT;
     int total = 0;
     for (int w0 = 0; w0 < items; w0 += 32)
       for (int bb = 0; bb < BPER; ++bb)
-        for (int wide = 0; wide < 2; ++wide) {
-          const int width = wide ? 8 : 16;  // lanes per wavefront
+        for (int plane = 0; plane < 2; ++plane) {
+          const int width = plane == 0 ? 8 : 16, mod = plane == 0 ? 8 : 16;
           for (int q0 = w0; q0 < w0 + 32 && q0 < items; q0 += width) {
             int cnt[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, worst = 0;
             for (int i = q0; i < q0 + width && i < items; ++i) {
               const int bg = i % L::BSPLIT, x = (i / L::BSPLIT) % 3, sl = (i / (3 * L::BSPLIT)) % 4;
-              const int alg = i / (12 * L::BSPLIT);  // (el, al)
+              const int alg = i / (12 * L::BSPLIT);  // (el, a')
               const int bp = bg * BPER + bb;
               if (bp >= S::NVE) continue;
-              const int off = alg * 4 * hs + sl * hs + bp * hb + x * 4;
-              const int k = wide ? (off / 2) % 8 : (off + 2) % 16;
+              const int k = (alg * 4 * hs2 + sl * hs2 + bp * hb2 + x) % mod;
               ++cnt[k];
               worst = worst > cnt[k] ? worst : cnt[k];
             }
@@ -248,23 +227,23 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
         }
     return total;
   }
-  static constexpr int hpick() {  // returns hb * 1024 + hs
+  static constexpr int hpick() {  // returns hb2 * 1024 + hs2
     long long best = 1LL << 62;
-    int pick = 12 * 1024 + S::NVE * 12;
-    for (int hb = 12; hb <= 24; hb += 2)
-      for (int pad = 0; pad < 16; pad += 2) {
-        const int hs = S::NVE * hb + pad;
-        // t'-major consumers read H warp-uniformly in b': only the stores matter there
-        const int cons = L::TMAJOR ? 1 : hconflicts(hb, hs);
-        const int prod = L::TMAJOR ? pwavefronts(hb, hs) : pconflicts(hb, hs);
-        const long long score = cons * 1000000000LL + prod * 10000LL + hs;  // then least memory
-        if (score < best) best = score, pick = hb * 1024 + hs;
+    int pick = 3 * 1024 + S::NVE * 3;
+    for (int hb2 = 3; hb2 <= 8; ++hb2)
+      for (int pad = 0; pad < 16; ++pad) {
+        const int hs2 = S::NVE * hb2 + pad;
+        // consumer loads weigh 4x: every consumer warp reads H, two producer warps write it
+        const long long score = (4LL * hwave_cons(hb2, hs2) + hwave_prod(hb2, hs2)) * 100000LL + hs2;
+        if (score < best) best = score, pick = hb2 * 1024 + hs2;
       }
     return pick;
   }
-  static constexpr int HB = hpick() / 1024;
-  static constexpr int HS = hpick() % 1024;
-  static constexpr int H_PER_BUF = L::EPC * L::AG * 4 * HS;
+  static constexpr int HPICK = hpick();
+  static constexpr int HB2 = HPICK / 1024;
+  static constexpr int HS2 = HPICK % 1024;
+  static constexpr int H2OFF = 2 * L::EPC * L::AG * 4 * HS2;  // the y = 2 plane
+  static constexpr int H_PER_BUF = (H2OFF + L::EPC * L::AG * 4 * HS2 + 1) / 2 * 2;
   static constexpr int NBUF = PI_SF_NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
   // Scalar forms build M for every point of the item up front (one wide,
   // latency-bound pass instead of one per chunk); systems (9 blocks per
@@ -520,9 +499,9 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           for (int bb = 0; bb < C::BPER; ++bb) {
             const int bp = bg * C::BPER + bb;
             if (bp < NVE) {
-              double* dst = Hb + ((el * AG + al) * 4 + sl) * C::HS + bp * C::HB + x * 4;
-              *reinterpret_cast<double2*>(dst) = make_double2(h[bb][0], h[bb][1]);
-              dst[2] = h[bb][2];
+              const int o = ((el * AG + al) * 4 + sl) * C::HS2 + bp * C::HB2 + x;
+              *reinterpret_cast<double2*>(Hb + 2 * o) = make_double2(h[bb][0], h[bb][1]);
+              Hb[C::H2OFF + o] = h[bb][2];
             }
           }
         }
@@ -588,7 +567,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
       // when NCB == 1, so b' and t' are resolved per item below for NCB > 1.
       const int j = ntl0[nb] * 8 + cpos;
       const int tp = j / NVE, b = j - tp * NVE;
-      hoff[nb] = b * C::HB;  // + x*4 at use
+      hoff[nb] = b * C::HB2;  // + (el, a', s) and x at use
       xoff0[nb] = tp;     // + s*3*NTPS at use
       const int tmax = min(NT - 1, (ntl0[nb] * 8 + 7) / NVE);
       unsigned m = 0;
@@ -661,9 +640,9 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           if constexpr (PAIRS) {
 #pragma unroll
             for (int pp = 0; pp < PPW; ++pp) {
-              const double* Hs = Hb + ((el_w * AG + pa[pp]) * 4 + sl_k[ks]) * C::HS + x_k[ks] * 4 + pb[pp] * C::HB;
-              const double2 h01 = *reinterpret_cast<const double2*>(Hs);
-              const double h2 = Hs[2];
+              const int o = ((el_w * AG + pa[pp]) * 4 + sl_k[ks]) * C::HS2 + x_k[ks] + pb[pp] * C::HB2;
+              const double2 h01 = *reinterpret_cast<const double2*>(Hb + 2 * o);
+              const double h2 = Hb[C::H2OFF + o];
 #pragma unroll
               for (int g = 0; g < MT; ++g) {
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
@@ -675,11 +654,11 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           } else {
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS + x_k[ks] * 4;
+            const int o = ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS2 + x_k[ks];
 #pragma unroll
             for (int b = 0; b < NVE; ++b) {
-              const double2 h01 = *reinterpret_cast<const double2*>(Hs + b * C::HB);
-              const double h2 = Hs[b * C::HB + 2];
+              const double2 h01 = *reinterpret_cast<const double2*>(Hb + 2 * (o + b * C::HB2));
+              const double h2 = Hb[C::H2OFF + o + b * C::HB2];
 #pragma unroll
               for (int g = 0; g < MT; ++g) {
                 const double gv = fma(h01.x, xv[g][0], fma(h01.y, xv[g][1], h2 * xv[g][2]));
@@ -705,15 +684,15 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
           }
 #pragma unroll
           for (int wa = 0; wa < WA; ++wa) {
-            const double* Hs = Hb + ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS + x_k[ks] * 4;
+            const int o = ((el_w * AG + al0 + wa) * 4 + sl_k[ks]) * C::HS2 + x_k[ks];
             // b' for n-tile nb is b'_(nb mod R): load each distinct one once
             double hr[C::RC][3];
 #pragma unroll
             for (int m = 0; m < C::RC; ++m) {
-              const double2 h01 = *reinterpret_cast<const double2*>(Hs + hoff[m]);
+              const double2 h01 = *reinterpret_cast<const double2*>(Hb + 2 * (o + hoff[m]));
               hr[m][0] = h01.x;
               hr[m][1] = h01.y;
-              hr[m][2] = Hs[hoff[m] + 2];
+              hr[m][2] = Hb[C::H2OFF + o + hoff[m]];
             }
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
