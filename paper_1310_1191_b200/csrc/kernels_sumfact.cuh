@@ -249,8 +249,11 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   // latency-bound pass instead of one per chunk); systems (9 blocks per
   // point) build it per chunk of 4 triangle points.
   static constexpr bool MALL = NE == 1;
-  static constexpr int MITEMS = L::EPC * (MALL ? S::NSP : 4) * S::NZ;  // points per M pass
-  static constexpr int MPITCH = MITEMS | 1;             // M stored k-major: [NE*NE][16][MPITCH]
+  // M stored k-major: [NE*NE][16][MPITCH], point (el, s, z) at el*MEL + s*NZ + z
+  // (an odd k-row pitch; padding MEL / MPITCH against the producers' read
+  // conflicts measured no gain).
+  static constexpr int MEL = (MALL ? S::NSP : 4) * S::NZ;  // points per element per M pass
+  static constexpr int MPITCH = (L::EPC * MEL) | 1;
   static constexpr int M_PER_CHUNK = NE * NE * 16 * MPITCH;
   static constexpr int NCOEF = 16 * NE * NE;            // coefficient tensor per element
   // shared memory layout (doubles; every block 16-byte aligned)
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
       for (int i = ptid; i < EPC * s_count * NZ; i += C::NPT) {
         const int z = i % NZ, sl = (i / NZ) % s_count, el = i / (s_count * NZ);
         const int s = s_first + sl;
-        double* Mi = sMb + i;
+        double* Mi = sMb + el * C::MEL + sl * NZ + z;
         if (s < NS) {
           double cf[3][3];
           const double det = jacobian_cofactors(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
           // M_k of point z at Mp[k*MPITCH + z]
-          const double* Mp = sM + mb * C::M_PER_CHUNK + (C::MALL ? (el * C::NSP + chunk * 4 + sl) : (el * 4 + sl)) * NZ;
+          const double* Mp = sM + mb * C::M_PER_CHUNK + el * C::MEL + (C::MALL ? chunk * 4 + sl : sl) * NZ;
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const double* Mz = Mp + z;
@@ -729,12 +732,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
       const int soff = bulk ? static_cast<int>((ecl * kk_elem) & amask) : 0;
       double* st = smem + C::OFF_STAGE + el_w * C::ESTRIDE + soff;
       float* stf = reinterpret_cast<float*>(smem + C::OFF_STAGE + el_w * C::ESTRIDE) + soff;
-      auto put = [&](int idx, double v) {
-        if (f32)
-          stf[idx] = static_cast<float>(v);
-        else
-          st[idx] = v;
-      };
+      auto stage = [&](auto put) {
       if constexpr (PAIRS) {
 #pragma unroll
         for (int pp = 0; pp < PPW; ++pp)
@@ -803,6 +801,13 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<
             }
           }
       }
+      };
+      stage([&](int idx, double v) {
+        if (f32)
+          stf[idx] = static_cast<float>(v);
+        else
+          st[idx] = v;
+      });
       fence_proxy_async_smem();
       named_sync(kBarCons, 32 * C::NCW);
       if (bulk) {

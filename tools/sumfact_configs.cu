@@ -6,9 +6,9 @@ using namespace pib;
 template <int P, int NE>
 void show() {
   using C = SumFactConfig<P, NE>;
-  std::printf("p=%d ne=%d tmajor=%d threads=%4d warps cons=%2d prod=%d smem=%7.1f KB  NTILE=%3d NBLK=%d NAG=%2d NCB=%d items/el=%3d acc=%d HB2=%d HS2=%d cons-wavefronts=%d prod-wavefronts=%d\n",
+  std::printf("p=%d ne=%d tmajor=%d threads=%4d warps cons=%2d prod=%d smem=%7.1f KB  NTILE=%3d NBLK=%d NAG=%2d NCB=%d MEL=%d MPITCH=%d items/el=%3d acc=%d HB2=%d HS2=%d cons-wavefronts=%d prod-wavefronts=%d\n",
               P, NE, (int)C::TMAJOR, C::NTHREADS, C::NCW, C::NPW, C::SMEM_BYTES / 1024.0, C::NTILE, C::NBLK, C::NAG,
-              C::NCB, C::NITEM, C::WA * C::MT * C::NB * 2, C::HB2, C::HS2, C::hwave_cons(C::HB2, C::HS2), C::hwave_prod(C::HB2, C::HS2));
+              C::NCB, C::MEL, C::MPITCH, C::NITEM, C::WA * C::MT * C::NB * 2, C::HB2, C::HS2, C::hwave_cons(C::HB2, C::HS2), C::hwave_prod(C::HB2, C::HS2));
 }
 int main() {
   show<2, 1>(); show<3, 1>(); show<4, 1>(); show<5, 1>(); show<6, 1>(); show<7, 1>();
