@@ -79,10 +79,12 @@ struct SumFactLaunch;
 // Per (p, n_eq): TMAJOR, EPC, AG, WA, NG, NBB, NB, NPW, BSPLIT, MINB, NCB.
 // Each can be overridden at build time (A/B runs, tools/ab_build.sh): a header
 // named by -DPI_SF_OVERRIDE (included by kernels_common.cuh) defining PI_SF_<p>_<n_eq>.
+// H ring depth per (p, n_eq): PI_SF_NBUF_<p>_<n_eq> (4 for p >= 4: +2 % at
+// p = 4), else PI_SF_NBUF (3: p = 3 keeps two CTAs per SM); 2..6 (named
+// barriers: FULL/EMPTY per buffer + 2 <= 16).
 #ifndef PI_SF_NBUF
 #define PI_SF_NBUF 3
 #endif
-static_assert(PI_SF_NBUF >= 2 && PI_SF_NBUF <= 6, "named barriers: FULL/EMPTY per buffer + 2 <= 16");
 #ifndef PI_SF_2_1
 #define PI_SF_2_1 true, 8, 3, 3, 1, 3, 3, 4, 1, 1, 1
 #endif
@@ -137,6 +139,47 @@ template <> struct SumFactLaunch<6, 3> : SumFactLaunchP<PI_SF_6_3> {};
 #define PI_SF_7_3 false, 1, 1, 1, 0, 0, 4, 2, 8, 1, 3
 #endif
 template <> struct SumFactLaunch<7, 3> : SumFactLaunchP<PI_SF_7_3> {};
+template <int P, int NE>
+struct SumFactNbuf {
+  static constexpr int value = PI_SF_NBUF;
+};
+#define PI_SF_NBUF_SPEC(p, ne, v) \
+  template <>                     \
+  struct SumFactNbuf<p, ne> {     \
+    static constexpr int value = v; \
+  };
+#ifndef PI_SF_NBUF_4_3
+#define PI_SF_NBUF_4_3 4
+#endif
+PI_SF_NBUF_SPEC(4, 3, PI_SF_NBUF_4_3)
+#ifndef PI_SF_NBUF_5_3
+#define PI_SF_NBUF_5_3 4
+#endif
+PI_SF_NBUF_SPEC(5, 3, PI_SF_NBUF_5_3)
+#ifndef PI_SF_NBUF_6_3
+#define PI_SF_NBUF_6_3 4
+#endif
+PI_SF_NBUF_SPEC(6, 3, PI_SF_NBUF_6_3)
+#ifndef PI_SF_NBUF_7_3
+#define PI_SF_NBUF_7_3 4
+#endif
+PI_SF_NBUF_SPEC(7, 3, PI_SF_NBUF_7_3)
+#ifndef PI_SF_NBUF_4_1
+#define PI_SF_NBUF_4_1 4
+#endif
+PI_SF_NBUF_SPEC(4, 1, PI_SF_NBUF_4_1)
+#ifndef PI_SF_NBUF_5_1
+#define PI_SF_NBUF_5_1 4
+#endif
+PI_SF_NBUF_SPEC(5, 1, PI_SF_NBUF_5_1)
+#ifndef PI_SF_NBUF_6_1
+#define PI_SF_NBUF_6_1 4
+#endif
+PI_SF_NBUF_SPEC(6, 1, PI_SF_NBUF_6_1)
+#ifndef PI_SF_NBUF_7_1
+#define PI_SF_NBUF_7_1 4
+#endif
+PI_SF_NBUF_SPEC(7, 1, PI_SF_NBUF_7_1)
 
 template <int P, int NE = 1>
 struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFactLaunch<P, NE> {
@@ -244,7 +287,8 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int HS2 = HPICK % 1024;
   static constexpr int H2OFF = 2 * L::EPC * L::AG * 4 * HS2;  // the y = 2 plane
   static constexpr int H_PER_BUF = (H2OFF + L::EPC * L::AG * 4 * HS2 + 1) / 2 * 2;
-  static constexpr int NBUF = PI_SF_NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
+  static constexpr int NBUF = SumFactNbuf<P, NE>::value;  // H ring depth (producers run up to NBUF chunks ahead)
+  static_assert(NBUF >= 2 && NBUF <= 6, "named barriers: FULL/EMPTY per buffer + 2 <= 16");
   // Scalar forms build M for every point of the item up front (one wide,
   // latency-bound pass instead of one per chunk); systems (9 blocks per
   // point) build it per chunk of 4 triangle points.
@@ -298,8 +342,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 // named barrier ids: FULL and EMPTY per ring buffer, producers, consumers
-constexpr int kBarFull0 = 1, kBarEmpty0 = 1 + PI_SF_NBUF, kBarProd = 1 + 2 * PI_SF_NBUF,
-              kBarCons = 2 + 2 * PI_SF_NBUF;
+constexpr int kBarFull0 = 1, kBarEmpty0 = 7, kBarProd = 13, kBarCons = 14;
 
 // Release fence for the shared-memory hand-off before bar.arrive (MEMBAR.ALL.CTA).
 __device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
