@@ -22,6 +22,13 @@
 
 namespace pib {
 
+#ifndef PI_PAIRS_NBUF  // H ring depth (p = 5: +3 %, p = 6: +1.4 % over 3)
+#define PI_PAIRS_NBUF 4
+#endif
+#ifndef PI_PAIRS_NBUF7  // p = 7: 4 buffers measured -1.5 %
+#define PI_PAIRS_NBUF7 3
+#endif
+
 template <int P, int NE>
 struct PairsConfig {
   using SF = SumFactConfig<P, NE>;  // shares the per-p tables (X fragments, X plain, Y, rule)
@@ -53,7 +60,7 @@ struct PairsConfig {
   // H ring: [PPI][4 s][3 x][HY] (HY = 4: y + pad; odd-ish s stride against bank conflicts)
   static constexpr int HX = 4, HSL = 3 * HX + 2, HPAIR = 4 * HSL + 2;
   static constexpr int H_PER_BUF = PPI * HPAIR;
-  static constexpr int NBUF = 3;
+  static constexpr int NBUF = P == 7 ? PI_PAIRS_NBUF7 : PI_PAIRS_NBUF;
   // M: all points of the element (scalar forms), double buffered across items
   static constexpr bool MALL = NE == 1;
   static constexpr int MITEMS = (MALL ? NSP : 4) * NZ;
