@@ -17,6 +17,7 @@ ap.add_argument("--p", type=int, default=4)
 ap.add_argument("--coeff", default="laplace", choices=["laplace", "cdr", "elasticity"])
 ap.add_argument("--nz", type=int, default=32)
 ap.add_argument("--reps", type=int, default=7)
+ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 dense, 2 sumfact")
 a = ap.parse_args()
 E = 2 * 128 * 64 * a.nz
 n_eq = 3 if a.coeff == "elasticity" else 1
@@ -30,7 +31,7 @@ elif mode == pb.ELASTICITY:
 dim = n_eq * pb.shape_count(a.p)
 chunk = min(E, int(100e9 / 8) // (dim * dim))
 out = torch.empty(chunk * dim * dim, dtype=torch.float64, device="cuda")
-it = pb.Integrator(a.p, n_eq=n_eq)
+it = pb.Integrator(a.p, n_eq=n_eq, variant=a.variant)
 s = torch.cuda.Stream()
 
 
@@ -56,4 +57,5 @@ it.check()
 ms = float(np.median(times))
 print(json.dumps({"lib": str(pb.LIB_PATH if not __import__("os").environ.get("PRISM_B200_LIB") else
                              __import__("os").environ["PRISM_B200_LIB"]),
-                  "p": a.p, "coeff": a.coeff, "elements": E, "ms": ms, "el_per_s": E / ms * 1e3}))
+                  "p": a.p, "coeff": a.coeff, "variant": a.variant, "elements": E, "ms": ms,
+                  "el_per_s": E / ms * 1e3}))
