@@ -155,8 +155,14 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
   const int64_t n_here = min(static_cast<int64_t>(kP1Threads), args.n_elem - first);
   const int total2 = static_cast<int>(n_here) * (KK / 2);
   if (args.out32) {
-    float2* dst = reinterpret_cast<float2*>(args.out32 + first * KK);
-    for (int i = tid; i < total2; i += kP1Threads) dst[i] = make_float2(static_cast<float>(so2[i].x), static_cast<float>(so2[i].y));
+    if ((reinterpret_cast<uintptr_t>(args.out32) & 7) == 0) {
+      float2* dst = reinterpret_cast<float2*>(args.out32 + first * KK);
+      for (int i = tid; i < total2; i += kP1Threads)
+        dst[i] = make_float2(static_cast<float>(so2[i].x), static_cast<float>(so2[i].y));
+    } else {  // 4-byte aligned output base
+      const double* so = sOut;
+      for (int i = tid; i < 2 * total2; i += kP1Threads) args.out32[first * KK + i] = static_cast<float>(so[i]);
+    }
   } else {
 #ifndef PI_P1_NO_BULK
     // the staging is the tile's exact global image: one TMA bulk store (16-byte
@@ -171,8 +177,12 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
       return;
     }
 #endif
-    double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
-    for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
+    if ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0) {
+      double2* dst = reinterpret_cast<double2*>(args.out + first * KK);
+      for (int i = tid; i < total2; i += kP1Threads) dst[i] = so2[i];
+    } else {  // 8-byte aligned output base
+      for (int i = tid; i < 2 * total2; i += kP1Threads) args.out[first * KK + i] = sOut[i];
+    }
   }
 }
 

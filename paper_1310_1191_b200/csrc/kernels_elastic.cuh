@@ -370,10 +370,8 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
         bulk_commit();
         bulk_wait_read();  // the next element's gradients overwrite the staging
       }
-    } else {
-      double2* dst = reinterpret_cast<double2*>(args.out + e * kE2KK);
-      const double2* src = reinterpret_cast<const double2*>(sw);
-      for (int r = lane; r < kE2KK / 2; r += 32) dst[r] = src[r];
+    } else {  // 8-byte aligned output base (kE2KK is even: every element keeps the base's alignment)
+      for (int r = lane; r < kE2KK; r += 32) args.out[e * kE2KK + r] = sw[r];
     }
     __syncwarp();  // staging read out before the next element's gradients overwrite it
   }
