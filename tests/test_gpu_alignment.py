@@ -55,3 +55,40 @@ def test_unaligned_output_same_bits(p, form, dtype):
     for shift in shifts:
         got = integrate(p, mesh, mode, coeff, n_eq, dtype, shift)
         assert np.array_equal(got, ref), (p, form, shift)
+
+
+def integrate_inputs(p, mesh, mode, coeff, n_eq, shift, extra):
+    """Geometry / coefficients read from SoA buffers starting `shift` doubles
+    into the allocation, with a row pitch of n + extra."""
+    n = len(mesh)
+    dim = n_eq * pb.shape_count(p)
+    ld = n + extra
+
+    def soa(aos):
+        aos = np.asarray(aos, dtype=np.float64).reshape(n, -1)
+        flat = np.full(shift + aos.shape[1] * ld, np.nan)
+        flat[shift:].reshape(aos.shape[1], ld)[:, :n] = aos.T
+        return torch.from_numpy(flat).cuda()[shift:]
+
+    g = soa(mesh.reshape(n, 18))
+    c = soa(coeff) if mode in (pb.PER_ELEMENT, pb.ELASTICITY) else None
+    out = torch.full((n, dim, dim), float("nan"), dtype=torch.float64, device="cuda")
+    with pb.Integrator(p, n_eq=n_eq) as it:
+        it.integrate_device(n, g, out, mode, c, geom_ld=ld, coeff_ld=ld if c is not None else None)
+        it.check()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("p,form", CASES)
+def test_shifted_strided_inputs_same_bits(p, form):
+    mesh = pb.generate_box_mesh(3, 2, 1, 0.2, seed=31 + p)
+    n = len(mesh)
+    n_eq, mode, coeff = 1, pb.LAPLACE, None
+    if form == "cdr":
+        mode, coeff = pb.PER_ELEMENT, pb.generate_cdr_coefficients(9, 0, n)
+    elif form == "elasticity":
+        n_eq, mode, coeff = 3, pb.ELASTICITY, pb.generate_materials(4, n)
+    ref = integrate_inputs(p, mesh, mode, coeff, n_eq, 0, 0)
+    assert np.isfinite(ref).all()
+    for shift, extra in ((1, 3), (3, 1)):
+        assert np.array_equal(integrate_inputs(p, mesh, mode, coeff, n_eq, shift, extra), ref), (shift, extra)
