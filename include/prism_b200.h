@@ -119,7 +119,10 @@ void* pi_context_stream(pi_context* ctx);                         /* cudaStream_
  * run_batch (kernels.hpp:68-75).
  *   geom   device SoA [18][geom_ld]
  *   coeff  see PI_COEFF_*; coeff_ld is the SoA leading dimension
- *   out    device, layout per out_layout (ld_out used by PI_OUT_SOA)     */
+ *   out    device, layout per out_layout (ld_out used by PI_OUT_SOA)
+ * Buffers need only element alignment (8 bytes, 4 for float32 output); a
+ * 16-byte aligned canonical output lets the kernels store whole element
+ * matrices with TMA bulk copies (tests/test_gpu_alignment.py).           */
 pi_status pi_integrate(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
                        int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld,
                        double* out, int out_layout, int64_t ld_out, void* stream, pi_error_info* err);
