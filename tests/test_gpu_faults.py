@@ -1,0 +1,51 @@
+"""Inverted-element detection in every kernel (geometry.cpp:67-69 raises
+InvertedElementError(element_id, xi, det) on det <= 0; kernels.cpp:158, 249
+report the global id base + local).  With several inverted elements the
+library reports the lowest global id (pi_check).  Fault injection as in the
+reference's verify.cpp:315-336: swap two vertices of an element."""
+import numpy as np
+import pytest
+
+import paper_1310_1191_b200 as pb
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FORMS = [(p, f) for f in ("laplace", "cdr", "elasticity") for p in range(1, 8)]
+
+
+def run(p, mesh, form, base, dtype=torch.float64):
+    n = len(mesh)
+    n_eq, mode, coeff = 1, pb.LAPLACE, None
+    if form == "cdr":
+        mode, coeff = pb.PER_ELEMENT, pb.generate_cdr_coefficients(2, 0, n)
+    elif form == "elasticity":
+        n_eq, mode, coeff = 3, pb.ELASTICITY, pb.generate_materials(2, n)
+    dim = n_eq * pb.shape_count(p)
+    g = torch.from_numpy(np.ascontiguousarray(mesh.reshape(n, 18).T)).cuda()
+    c = None if coeff is None else torch.from_numpy(np.ascontiguousarray(np.asarray(coeff).reshape(n, -1).T)).cuda()
+    out = torch.empty((n, dim, dim), dtype=dtype, device="cuda")
+    with pb.Integrator(p, n_eq=n_eq) as it:
+        it.integrate_device(n, g, out, mode, c, element_id_base=base)
+        it.check()
+    return out
+
+
+@pytest.mark.parametrize("p,form", FORMS)
+def test_lowest_inverted_global_id(p, form):
+    mesh = pb.generate_box_mesh(3, 2, 1, 0.1, seed=p).copy()
+    for e in (9, 4):
+        mesh[e, [1, 2]] = mesh[e, [2, 1]]
+    with pytest.raises(pb.InvertedElementError) as ei:
+        run(p, mesh, form, base=7000)
+    assert ei.value.element == 7004
+    assert ei.value.det <= 0.0
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_inverted_detected_in_f32_variant(p):
+    mesh = pb.generate_box_mesh(2, 2, 1, 0.1, seed=1).copy()
+    mesh[5, [0, 1]] = mesh[5, [1, 0]]
+    with pytest.raises(pb.InvertedElementError) as ei:
+        run(p, mesh, "laplace", base=0, dtype=torch.float32)
+    assert ei.value.element == 5
