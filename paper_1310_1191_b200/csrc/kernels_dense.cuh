@@ -25,6 +25,9 @@ template <bool GENERAL>
 constexpr int p1_threads() {
   return GENERAL ? 64 : 128;
 }
+#ifndef PI_P1_MINB  // CTAs per SM of the Laplace thread kernel
+#define PI_P1_MINB 4
+#endif
 #ifndef PI_P1_MINB_GENERAL
 #define PI_P1_MINB_GENERAL 2
 #endif
@@ -54,7 +57,7 @@ struct BasisPattern {
 // skipped at compile time (13 of the 24 phi entries per point are non-zero),
 // so the contraction costs about half the dense loop nest's FMAs.
 template <bool GENERAL>
-__global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : 4)
+__global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : PI_P1_MINB)
     p1_thread_kernel(LaunchArgs args, DenseTables tab) {
   constexpr int kP1Threads = p1_threads<GENERAL>();
   constexpr int NQ = 6, NSH = 6, KK = NSH * NSH;
