@@ -49,3 +49,30 @@ def test_inverted_detected_in_f32_variant(p):
     with pytest.raises(pb.InvertedElementError) as ei:
         run(p, mesh, "laplace", base=0, dtype=torch.float32)
     assert ei.value.element == 5
+
+
+@pytest.mark.parametrize("n_eq", [1, 3])
+def test_empty_batch_is_a_no_op(n_eq):
+    """n_elem = 0: PI_OK, nothing written (every p, both precisions)."""
+    for p in range(1, 8):
+        dim = n_eq * pb.shape_count(p)
+        g = torch.zeros((18, 1), dtype=torch.float64, device="cuda")
+        for dtype in (torch.float64, torch.float32):
+            out = torch.full((dim * dim,), 7.0, dtype=dtype, device="cuda")
+            with pb.Integrator(p, n_eq=n_eq) as it:
+                mode = pb.LAPLACE if n_eq == 1 else pb.ELASTICITY_UNIFORM
+                coeff = None if n_eq == 1 else np.array([1.0, 0.3])
+                it.integrate_device(0, g, out, mode, coeff)
+                it.check()
+            assert bool((out == 7.0).all())
+
+
+@pytest.mark.parametrize("form", ["cdr", "elasticity"])
+def test_single_and_odd_counts(form):
+    """1, 2 and 37 elements through every kernel of the weak form: each equals the full-batch result."""
+    mesh = pb.generate_box_mesh(4, 3, 2, 0.15, seed=8)
+    for p in range(1, 8):
+        full = run(p, mesh[:37], form, base=0).cpu()
+        for n in (1, 2):
+            # coefficients / materials are pure functions of the element id
+            assert torch.equal(run(p, mesh[:n], form, base=0).cpu(), full[:n])
