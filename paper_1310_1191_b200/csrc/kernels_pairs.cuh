@@ -14,7 +14,8 @@
 //     G = sum_y H_xy(s, a', b') X_y(t', s),     t' = 8 g + lane/4,
 // so only H for the item's own pairs is formed by the producers (no H for
 // a' > b').  Blocks are stored straight from registers together with their
-// mirrors; an element's rows are written by several CTAs and merge in L2.
+// mirrors; a CTA walks all pair items of its element, whose 32-byte sectors
+// are completed across items and merge in L2.
 // About 56 % of the MMAs and fragment FMAs of the row split.
 #pragma once
 
