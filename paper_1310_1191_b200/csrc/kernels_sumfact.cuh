@@ -112,11 +112,11 @@ template <> struct SumFactLaunch<7, 1> : SumFactLaunchP<PI_SF_7_1> {};
 // n_eq = 3 (elasticity): K is 9x larger; p >= 6 also splits columns over CTAs
 // (column blocks of whole t' rows: 42 tiles = 16 t' at p = 6, 36 = 12 at p = 7).
 #ifndef PI_SF_1_3
-#define PI_SF_1_3 false, 2, 6, 3, 0, 0, 3, 2, 2, 2, 1
+#define PI_SF_1_3 false, 2, 6, 3, 0, 0, 3, 2, 2, 1, 1
 #endif
 template <> struct SumFactLaunch<1, 3> : SumFactLaunchP<PI_SF_1_3> {};
 #ifndef PI_SF_2_3
-#define PI_SF_2_3 false, 1, 9, 3, 0, 0, 7, 2, 3, 2, 1
+#define PI_SF_2_3 false, 1, 9, 3, 0, 0, 7, 2, 3, 1, 1
 #endif
 template <> struct SumFactLaunch<2, 3> : SumFactLaunchP<PI_SF_2_3> {};
 #ifndef PI_SF_3_3

@@ -181,3 +181,23 @@ def test_elasticity_soa_layout(p):
         it.check()
     soa = out.cpu().numpy()[:, :n].T.reshape(n, dim, dim)
     assert np.array_equal(soa, canon)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_sumfact_variant_at_low_p(p):
+    """The DMMA sum-factorisation strategy (pi_context_set_variant SUMFACT) for
+    n_eq = 3 at p <= 3, where the default is the dense lane / warp / CTA kernels."""
+    mesh = pb.generate_box_mesh(2, 2, 1, 0.2, seed=60 + p)
+    n = len(mesh)
+    mats = materials(n, 60 + p)
+    dim = 3 * pb.shape_count(p)
+    g = torch.from_numpy(np.ascontiguousarray(mesh.reshape(n, 18).T)).cuda()
+    c = torch.from_numpy(np.ascontiguousarray(mats.T)).cuda()
+    res = {}
+    for v in (pb.VARIANT_DENSE, pb.VARIANT_SUMFACT):
+        out = torch.full((n, dim, dim), float("nan"), dtype=torch.float64, device="cuda")
+        with pb.Integrator(p, n_eq=3, variant=v) as it:
+            it.integrate_device(n, g, out, pb.ELASTICITY, c)
+            it.check()
+        res[v] = out.cpu().numpy()
+    assert rel_frobenius(res[pb.VARIANT_DENSE], res[pb.VARIANT_SUMFACT], axis=(1, 2)).max() <= TOL

@@ -6,8 +6,8 @@ using namespace pib;
 template <int P, int NE>
 void show() {
   using C = SumFactConfig<P, NE>;
-  std::printf("p=%d ne=%d tmajor=%d threads=%4d warps cons=%2d prod=%d smem=%7.1f KB  NTILE=%3d NBLK=%d NAG=%2d NCB=%d MEL=%d MPITCH=%d items/el=%3d acc=%d HB2=%d HS2=%d cons-wavefronts=%d prod-wavefronts=%d\n",
-              P, NE, (int)C::TMAJOR, C::NTHREADS, C::NCW, C::NPW, C::SMEM_BYTES / 1024.0, C::NTILE, C::NBLK, C::NAG,
+  std::printf("p=%d ne=%d tmajor=%d threads=%4d warps cons=%2d prod=%d smem=%7.1f KB minb=%d nbuf=%d NTILE=%3d NBLK=%d NAG=%2d NCB=%d MEL=%d MPITCH=%d items/el=%3d acc=%d HB2=%d HS2=%d cons-wavefronts=%d prod-wavefronts=%d\n",
+              P, NE, (int)C::TMAJOR, C::NTHREADS, C::NCW, C::NPW, C::SMEM_BYTES / 1024.0, C::MINB, C::NBUF, C::NTILE, C::NBLK, C::NAG,
               C::NCB, C::MEL, C::MPITCH, C::NITEM, C::WA * C::MT * C::NB * 2, C::HB2, C::HS2, C::hwave_cons(C::HB2, C::HS2), C::hwave_prod(C::HB2, C::HS2));
 }
 int main() {
