@@ -181,10 +181,35 @@ PI_SF_NBUF_SPEC(6, 1, PI_SF_NBUF_6_1)
 #endif
 PI_SF_NBUF_SPEC(7, 1, PI_SF_NBUF_7_1)
 
-template <int P, int NE = 1>
-struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFactLaunch<P, NE> {
-  using S = SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>;
-  using L = SumFactLaunch<P, NE>;
+// Symmetric forms may take their own launch shape and ring depth
+// (PI_SF_<p>_<ne>_SYM): p = 4 Laplace runs one element per CTA at two CTAs
+// per SM (+1.2 %), a shape that costs the general (CDR) form 5 %.  Both
+// shapes of a (p, n_eq) must share the per-p tables (same TMAJOR).
+template <int P, int NE>
+struct SumFactLaunchSym : SumFactLaunch<P, NE> {
+  static constexpr int NBUF = SumFactNbuf<P, NE>::value;
+};
+#ifndef PI_SF_4_1_SYM
+#define PI_SF_4_1_SYM true, 1, 5, 1, 2, 5, 10, 1, 1, 2, 1
+#endif
+#ifndef PI_SF_NBUF_4_1_SYM
+#define PI_SF_NBUF_4_1_SYM 3
+#endif
+template <>
+struct SumFactLaunchSym<4, 1> : SumFactLaunchP<PI_SF_4_1_SYM> {
+  static constexpr int NBUF = PI_SF_NBUF_4_1_SYM;
+};
+template <int P, int NE, bool SYMV>
+struct SumFactLaunchSel : SumFactLaunch<P, NE> {
+  static constexpr int NBUF = SumFactNbuf<P, NE>::value;
+};
+template <int P, int NE>
+struct SumFactLaunchSel<P, NE, true> : SumFactLaunchSym<P, NE> {};
+
+template <int P, int NE = 1, bool SYMV = false>
+struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR>, SumFactLaunchSel<P, NE, SYMV> {
+  using S = SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR>;
+  using L = SumFactLaunchSel<P, NE, SYMV>;
   // n-tiles of 8 columns: t'-major (g, b') tiles, or natural tiles padded to
   // a whole number of NB x NCB blocks (padding columns are computed from
   // zero X rows and never stored)
@@ -287,7 +312,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunch<P, NE>::TMAJOR>, SumFac
   static constexpr int HS2 = HPICK % 1024;
   static constexpr int H2OFF = 2 * L::EPC * L::AG * 4 * HS2;  // the y = 2 plane
   static constexpr int H_PER_BUF = (H2OFF + L::EPC * L::AG * 4 * HS2 + 1) / 2 * 2;
-  static constexpr int NBUF = SumFactNbuf<P, NE>::value;  // H ring depth (producers run up to NBUF chunks ahead)
+  static constexpr int NBUF = L::NBUF;  // H ring depth (producers run up to NBUF chunks ahead)
   static_assert(NBUF >= 2 && NBUF <= 6, "named barriers: FULL/EMPTY per buffer + 2 <= 16");
   // Scalar forms build M for every point of the item up front (one wide,
   // latency-bound pass instead of one per chunk); systems (9 blocks per
@@ -352,9 +377,9 @@ __device__ __forceinline__ void smem_release() { asm volatile("fence.acq_rel.cta
 // blocks with t'-block >= t-block are multiplied; the rest are mirrored
 // from the CTA's staged K.
 template <int P, int NE, int FORM, bool SYM>
-__global__ void __launch_bounds__(SumFactConfig<P, NE>::NTHREADS, SumFactConfig<P, NE>::MINB)
+__global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactConfig<P, NE, SYM>::MINB)
     sumfact_kernel(LaunchArgs args, SumFactTables tab) {
-  using C = SumFactConfig<P, NE>;
+  using C = SumFactConfig<P, NE, SYM>;
   constexpr bool GENERAL = FORM == kFormGeneral;  // value row/column present in M
   constexpr bool SYMK = SYM && C::TMAJOR && C::NAG == 1;
   // Symmetric t'-major with one warp per vertical row (WPE == NVE, odd): the

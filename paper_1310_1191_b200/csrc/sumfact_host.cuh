@@ -13,11 +13,16 @@ namespace pib {
 
 template <int P, int NE>
 struct SumFactHost {
-  using C = SumFactConfig<P, NE>;
+  using C = SumFactConfig<P, NE>;         // tables; the general-form kernels
+  using CS = SumFactConfig<P, NE, true>;  // the symmetric-form kernels
+  static_assert(C::TMAJOR == CS::TMAJOR && C::XPLAIN == CS::XPLAIN && C::XFRAG == CS::XFRAG,
+                "both launch shapes of a (p, n_eq) read the same tables");
+  template <bool SYM>
+  using CK = SumFactConfig<P, NE, SYM>;
   template <int FORM, bool SYM>
   static void attr() {
     cudaFuncSetAttribute(sumfact_kernel<P, NE, FORM, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(C::SMEM_BYTES));
+                         static_cast<int>(CK<SYM>::SMEM_BYTES));
   }
   // Persistent grid: as many CTAs as fit on the device at once (queried per
   // instantiation), each looping over (element group, a'-group, column block) items.
@@ -28,8 +33,8 @@ struct SumFactHost {
       int dev = 0, sms = 0, per_sm = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, NE, FORM, SYM>, C::NTHREADS,
-                                                    C::SMEM_BYTES);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, NE, FORM, SYM>, CK<SYM>::NTHREADS,
+                                                    CK<SYM>::SMEM_BYTES);
       c = std::max(1, sms * std::max(1, per_sm));
     }
     return c;
@@ -72,9 +77,10 @@ struct SumFactHost {
     if constexpr (SYM)
       if (go_pairs<FORM>(a, t, s)) return;
 #endif
-    const int64_t items = (a.n_elem + C::EPC - 1) / C::EPC * C::NITEM;
+    using K = CK<SYM>;
+    const int64_t items = (a.n_elem + K::EPC - 1) / K::EPC * K::NITEM;
     const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<FORM, SYM>())));
-    sumfact_kernel<P, NE, FORM, SYM><<<grid, C::NTHREADS, C::SMEM_BYTES, s>>>(a, t);
+    sumfact_kernel<P, NE, FORM, SYM><<<grid, K::NTHREADS, K::SMEM_BYTES, s>>>(a, t);
   }
 
   // Builds the X fragment table, Y table and rule coordinates from the
@@ -151,30 +157,30 @@ struct SumFactHost {
   // (t'-major skips t'-blocks below the t-block; natural order skips n-tiles
   // whose largest t' lies below the m-tile).
   static double sym_fraction() {
-    if (C::NAG != 1 || C::NCB != 1) return 1.0;
-    if (C::PAIRS) {
+    if (CS::NAG != 1 || CS::NCB != 1) return 1.0;
+    if (CS::PAIRS) {
       // (a', b') pairs with a' <= b' (kernels_sumfact.cuh PAIRS)
-      const double mt = C::MT, nve = C::NVE;
+      const double mt = CS::MT, nve = CS::NVE;
       return (nve * mt * (mt + 1) / 2 + nve * (nve - 1) / 2 * mt * mt) / (nve * nve * mt * mt);
     }
     long done = 0;
-    for (int t = 0; t < C::NT; ++t)
-      for (int tp = 0; tp < C::NT; ++tp) {
+    for (int t = 0; t < CS::NT; ++t)
+      for (int tp = 0; tp < CS::NT; ++tp) {
         const int mt = t / 8;
         bool comp;
-        if (C::TMAJOR) {
+        if (CS::TMAJOR) {
           comp = tp / 8 >= mt;
         } else {
-          const int nt = (tp * C::NVE) / 8;
-          comp = std::min(C::NT - 1, (nt * 8 + 7) / C::NVE) >= 8 * mt;
+          const int nt = (tp * CS::NVE) / 8;
+          comp = std::min(CS::NT - 1, (nt * 8 + 7) / CS::NVE) >= 8 * mt;
         }
         done += comp;
       }
-    return static_cast<double>(done) / (C::NT * C::NT);
+    return static_cast<double>(done) / (CS::NT * CS::NT);
   }
   // fraction of the B-fragment values the symmetric path forms (PAIRS: a' <= b')
   static double fragment_fraction() {
-    if (C::PAIRS) return (C::NVE + 1) / (2.0 * C::NVE);
+    if (CS::PAIRS) return (CS::NVE + 1) / (2.0 * CS::NVE);
     return 1.0;
   }
   static void padded(int& cols, int& rows, int& k4) {
