@@ -183,7 +183,8 @@ PI_SF_NBUF_SPEC(7, 1, PI_SF_NBUF_7_1)
 
 // Symmetric forms may take their own launch shape and ring depth
 // (PI_SF_<p>_<ne>_SYM): p = 4 Laplace runs one element per CTA at two CTAs
-// per SM (+1.2 %), a shape that costs the general (CDR) form 5 %.  Both
+// per SM (+1.2 %), a shape that costs the general (CDR) form 5 %; p = 3
+// splits the producers' H items over two b' halves.  Both
 // shapes of a (p, n_eq) must share the per-p tables (same TMAJOR).
 template <int P, int NE>
 struct SumFactLaunchSym : SumFactLaunch<P, NE> {
@@ -198,6 +199,13 @@ struct SumFactLaunchSym : SumFactLaunch<P, NE> {
 template <>
 struct SumFactLaunchSym<4, 1> : SumFactLaunchP<PI_SF_4_1_SYM> {
   static constexpr int NBUF = PI_SF_NBUF_4_1_SYM;
+};
+#ifndef PI_SF_3_1_SYM  // H items split over two b' halves: Laplace +1.6 %, CDR -1.7 %
+#define PI_SF_3_1_SYM false, 2, 4, 2, 0, 0, 5, 2, 2, 2, 1
+#endif
+template <>
+struct SumFactLaunchSym<3, 1> : SumFactLaunchP<PI_SF_3_1_SYM> {
+  static constexpr int NBUF = SumFactNbuf<3, 1>::value;
 };
 template <int P, int NE, bool SYMV>
 struct SumFactLaunchSel : SumFactLaunch<P, NE> {

@@ -28,7 +28,7 @@ def configs(tmp_path_factory):
     for line in out.splitlines():
         kv = dict(re.findall(r"([\w/-]+)=\s*([\d.]+)", line))
         rows.append(kv)
-    assert len(rows) == 14  # 13 (p, n_eq) shapes + the symmetric p = 4 shape
+    assert len(rows) == 15  # 13 (p, n_eq) shapes + the symmetric p = 3, 4 shapes
     return rows
 
 

@@ -13,5 +13,5 @@ void show() {
 int main() {
   show<2, 1>(); show<3, 1>(); show<4, 1>(); show<5, 1>(); show<6, 1>(); show<7, 1>();
   show<1, 3>(); show<2, 3>(); show<3, 3>(); show<4, 3>(); show<5, 3>(); show<6, 3>(); show<7, 3>();
-  show<4, 1, true>();
+  show<3, 1, true>(); show<4, 1, true>();
 }
