@@ -2,30 +2,45 @@
 """Benchmark: element stiffness integration for prisms (arXiv 1310.1191) on B200.
 
 Metric (BASELINE.json): elements integrated per second per degree p, plus the
-fraction of the FP64 / HBM roofline.  Workload (BASELINE.json configs[1]):
-Laplace weak form, p = 2, 3, 4, 1,048,576 synthetic prisms per GPU
-(generate_box_mesh(128, 64, 64*N, 0.1, 42), rank r owns the contiguous range
-[r*E, (r+1)*E) -- weak scaling, no collective on the data path).
+fraction of the FP64 / HBM roofline.
 
-One step = one pass of the hot path over the rank's elements at every p in
---p (three launches of the sm_100a kernels, outputs device-resident).
-value = elements processed by all ranks in the timed steps / max-over-ranks
-device time.  e2e = the same step through the host-buffer C-ABI call
-(pi_integrate_host): pinned host geometry in, pinned host K out, all copies
-inside the timed region.
+Headline workload (BASELINE.json configs[1]): Laplace weak form, p = 2, 3, 4,
+1,048,576 synthetic prisms per GPU.  One step = one pass of the hot path over
+the rank's elements at every p (outputs device-resident).  `value` = elements
+processed by all ranks in the timed steps / max-over-ranks device time.
 
-  python bench.py [--gpus N --steps K --warmup W --p 2,3,4 --coeff laplace|cdr]
-  python bench.py --impl reference ...   # the reference CPU integrate_generic
+  --scaling weak   (default) generate_box_mesh(128, 64, 64*N, 0.1, 42); rank r
+                   owns the contiguous range [r*E, (r+1)*E), E = 1,048,576.
+  --scaling strong generate_box_mesh(256, 256, 128, 0.1, 42) = 16,777,216
+                   prisms (BASELINE configs[4]) split into N contiguous ranges
+                   [floor(rT/N), floor((r+1)T/N)).  No collective on the data path.
+
+Beside the headline the line carries
+  * `sweep`: every p = 1..7 for Laplace and per-element CDR (configs[2], [3])
+    over the same per-rank elements, median of --reps event-timed passes, with
+    executed-FP64 / HBM / dense-count roofline fractions and parity samples;
+  * `parity`: SURVEY.md 8(d) sample counts (256 at p <= 4, 64 at p = 5, 16 at
+    p >= 6, evenly spaced `sample_indices`, verify.cpp:50-59) against the
+    reference's integrate_generic, plus a placement check (each sampled element
+    re-integrated alone is bitwise equal) and a digest of the sampled matrices
+    (equal across N in strong scaling);
+  * `e2e`: the same step through the host-buffer C-ABI call (pi_integrate_host:
+    pinned host geometry in, pinned host K out, all copies timed);
+  * `cpu_baseline`: the reference's integrate_generic (oracle/_ref) on the
+    host cores (all threads, plus a 1-core figure) over a bounded sample.
+
+  python bench.py [--gpus N --steps K --warmup W --p 2,3,4 --coeff laplace|cdr|elasticity]
+  python bench.py --impl reference ...   # the reference CPU integrate_generic, same config
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -35,28 +50,56 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "elements integrated/sec per degree p (1 and 8 B200) and % of FP64/HBM roofline"
-NX, NY, NZ_PER_RANK, DISTORTION, SEED = 128, 64, 64, 0.1, 42
-COEFF_SEED = 42
+WEAK_MESH = (128, 64, 64)      # per rank: 2*128*64*64 = 1,048,576 prisms
+STRONG_MESH = (256, 256, 128)  # 16,777,216 prisms in total
+DISTORTION, SEED, COEFF_SEED = 0.1, 42, 42
+FORMS = {"laplace": 0, "cdr": 2, "elasticity": 3}  # PI_COEFF_* of the weak form
 
 
-def parse():
+def sample_count(p: int) -> int:
+    """Parity sample per p."""
+    return 256 if p <= 4 else 64 if p == 5 else 16
+
+
+def sample_indices(n: int, want: int):
+    """verify.cpp:50-59: evenly spaced sample."""
+    if n == 0:
+        return []
+    want = min(want, n)
+    return [0 if want == 1 else i * (n - 1) // (want - 1) for i in range(want)]
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", default="2,3,4")
-    ap.add_argument("--coeff", default="laplace", choices=["laplace", "cdr", "elasticity"],
+    ap.add_argument("--coeff", default="laplace", choices=list(FORMS),
                     help="weak form: Laplace, per-element CDR tensors, or n_eq=3 elasticity with per-element (E, nu)")
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
-                    help="K output precision (f32: the FP32 output variant, SURVEY 8f row f3)")
+                    help="f32: the FP32 variant (SURVEY 8f row f3), K in float32")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--mesh", default=None,
+                    help="NX,NY,NZ: per-rank box (weak, NZ multiplied by N) or the whole box (strong)")
     ap.add_argument("--out-gb", type=float, default=120.0,
-                    help="device output budget; larger steps stream through a ring of chunks")
-    ap.add_argument("--nz", type=int, default=NZ_PER_RANK, help="mesh layers per rank (64 -> 1M elements)")
+                    help="device output budget per GPU; larger passes stream through it chunk by chunk")
+    ap.add_argument("--sweep", default="laplace,cdr", help="weak forms of the p-sweep ('' disables)")
+    ap.add_argument("--sweep-p", default="1,2,3,4,5,6,7")
+    ap.add_argument("--reps", type=int, default=3, help="timed passes per sweep entry (median reported)")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=18.0, help="CPU baseline budget")
-    return ap.parse_args()
+    ap.add_argument("--cpu-seconds", type=float, default=16.0, help="CPU baseline budget (all threads)")
+    ap.add_argument("--cpu1-seconds", type=float, default=4.0, help="CPU baseline budget (1 thread)")
+    ap.add_argument("--csv", default=None, help="also write the reference's bench CSV rows (bench.cpp:136-141)")
+    # legacy spelling of the per-rank layer count
+    ap.add_argument("--nz", type=int, default=None, help=argparse.SUPPRESS)
+    a = ap.parse_args(argv)
+    if a.nz is not None and a.mesh is None:
+        a.mesh = f"{WEAK_MESH[0]},{WEAK_MESH[1]},{a.nz}"
+    return a
 
 
 def dist_env():
@@ -66,30 +109,73 @@ def dist_env():
     return ws, rank, local
 
 
+class Workload:
+    """Mesh, this rank's contiguous element range and the config dict both arms print."""
+
+    def __init__(self, args, ws, rank):
+        self.scaling = args.scaling
+        self.ps = [int(x) for x in args.p.split(",")]
+        self.coeff = args.coeff
+        if args.scaling == "weak":
+            nx, ny, nz = (int(v) for v in args.mesh.split(",")) if args.mesh else WEAK_MESH
+            self.mesh = (nx, ny, nz * ws)
+            self.total = 2 * nx * ny * nz * ws
+            self.E = 2 * nx * ny * nz
+            self.first = rank * self.E
+        else:
+            self.mesh = tuple(int(v) for v in args.mesh.split(",")) if args.mesh else STRONG_MESH
+            self.total = 2 * self.mesh[0] * self.mesh[1] * self.mesh[2]
+            self.first = rank * self.total // ws                       # partition.rank_range
+            self.E = (rank + 1) * self.total // ws - self.first
+        self.ws = ws
+        self.precision = args.precision
+        self.n_eq = 3 if args.coeff == "elasticity" else 1
+
+    def config(self):
+        nx, ny, nz = self.mesh
+        form = {"laplace": "Laplace c=I", "cdr": "seeded per-element CDR tensors",
+                "elasticity": "n_eq=3 isotropic elasticity, per-element (E, nu)"}[self.coeff]
+        tag = ""
+        if self.coeff == "laplace" and self.ps == [2, 3, 4] and self.scaling == "weak":
+            tag = " (BASELINE configs[1])"
+        per = "per GPU" if self.scaling == "weak" else f"in total over {self.ws} GPU(s)"
+        n = self.E if self.scaling == "weak" else self.total
+        return {"workload": f"{self.coeff} p={','.join(map(str, self.ps))}, {n} prisms {per}{tag}",
+                "mesh": f"generate_box_mesh({nx}, {ny}, {nz}, {DISTORTION}, {SEED})", "weak_form": form,
+                "elements_per_gpu": self.E if self.scaling == "weak" else None, "total_elements": self.total,
+                "p": self.ps, "coeff": self.coeff, "n_eq": self.n_eq, "precision": self.precision,
+                "parallelism": f"element-range x{self.ws}", "scaling": self.scaling,
+                "l2": "no flush needed: inputs (151 MB geometry per 1M prisms) and outputs (GBs) exceed the 126 MB L2"}
+
+    def data(self):
+        return (f"synthetic: generate_box_mesh{self.mesh} distortion {DISTORTION} seed {SEED} (the reference's "
+                f"generator, geometry.cpp:134-201); coefficients seeded per element ({self.coeff})")
+
+
 # ----------------------------------------------------------------- CPU legs
-def cpu_reference_rates(ps, coeff_kind, budget_s, mesh_aos, coeffs_aos):
-    """Reference integrate_generic (oracle/_ref, all host threads) el/s per p on a
-    bounded sample of the same mesh -- integrate_optimized, the reference's
-    fastest FP64 path, for elasticity.  Returns (rates, sample description, cores, kind)."""
+def cpu_reference_rates(ps, coeff_kind, budget_s, mesh_aos, coeffs_aos, threads=0):
+    """Reference integrate_generic (oracle/_ref) el/s per p on a bounded sample of
+    the same mesh -- integrate_optimized, the reference's fastest FP64 path, for
+    elasticity.  threads 0 = all host threads.  Returns (rates, samples, cores, kind)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import REF_SO, Oracle, Reference, laplace_tensor  # test infrastructure (checker)
 
-    cores = os.cpu_count() or 1
+    cores = (os.cpu_count() or 1) if threads <= 0 else threads
     kind = "reference" if REF_SO.exists() else "port"
     rates, samples = {}, {}
     per_p = budget_s / max(1, len(ps))
     for p in ps:
-        n = 16
+        n = 4
         while True:
             g = mesh_aos[:n]
-            c = laplace_tensor() if coeff_kind == "laplace" else (coeffs_aos[:n] if coeffs_aos is not None else None)
+            c = laplace_tensor() if coeff_kind == "laplace" else coeffs_aos[:n]
             t0 = time.perf_counter()
             if coeff_kind == "elasticity":
                 if kind == "reference":
-                    Reference().integrate_optimized_batch(p, g, coeffs_aos[:n], threads=cores)
+                    Reference().integrate_optimized_batch(p, g, c, threads=cores)
                 else:
                     o = Oracle()
-                    o.integrate_batch(p, g, np.stack([o.elasticity_tensor(*m) for m in coeffs_aos[:n]]), n_eq=3)
+                    o.integrate_batch(p, g, np.stack([o.elasticity_tensor(*m) for m in c]), n_eq=3)
             elif kind == "reference":
                 _, err = Reference().integrate_batch(p, g, c, threads=cores)
                 assert err is None
@@ -101,13 +187,38 @@ def cpu_reference_rates(ps, coeff_kind, budget_s, mesh_aos, coeffs_aos):
             n = min(len(mesh_aos), int(n * max(2.0, per_p * 0.3 / max(dt, 1e-4))))
         rates[p] = n / dt
         samples[p] = n
-    desc = ", ".join(f"p={p}: first {samples[p]} elements" for p in ps)
-    return rates, desc, cores if kind == "reference" else 1, kind
+    return rates, samples, cores if kind == "reference" else 1, kind
 
 
 def step_rate(rates, ps):
     """Elements/s of one step (E elements at every p) from per-p rates."""
     return len(ps) / sum(1.0 / rates[p] for p in ps)
+
+
+def checker(p, mode, geoms, coeffs, threads=0):
+    """The reference's own arithmetic on sampled elements (oracle/_ref), else the C port."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import REF_SO, Oracle, Reference, laplace_tensor
+
+    if mode == FORMS["elasticity"]:
+        if REF_SO.exists():
+            return Reference().integrate_optimized_batch(p, geoms, coeffs, threads=threads)
+        o = Oracle()
+        return o.integrate_batch(p, geoms, np.stack([o.elasticity_tensor(*m) for m in coeffs]), n_eq=3)
+    c = laplace_tensor() if mode == FORMS["laplace"] else coeffs
+    if REF_SO.exists():
+        out, err = Reference().integrate_batch(p, geoms, c, threads=threads)
+        assert err is None, err.message
+        return out
+    return Oracle().integrate_batch(p, geoms, c)
+
+
+def checker_name(mode):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import REF_SO
+
+    fn = "integrate_optimized" if mode == FORMS["elasticity"] else "integrate_generic"
+    return f"reference {fn} (oracle/_ref)" if REF_SO.exists() else f"oracle port of {fn}"
 
 
 # ------------------------------------------------------------------ clocks
@@ -165,253 +276,410 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def peaks_hbm():
+    """HBM denominator: the driver's MEASURED_PEAKS.json, else the committed copy
+    of this pool's measurement (profiles/measured_peaks_pool.json), else the
+    B200_PROFILING.md fallback."""
+    for path, tag in ((ROOT / "MEASURED_PEAKS.json", "of measured (MEASURED_PEAKS.json)"),
+                      (ROOT / "profiles" / "measured_peaks_pool.json",
+                       "of measured (this pool's MEASURED_PEAKS.json, committed copy)")):
+        try:
+            return float(json.load(open(path))["hbm_gbs"]), tag
+        except Exception:
+            continue
+    return 6650.0, "of fallback (B200_PROFILING.md)"
+
+
 # ------------------------------------------------------------ reference arm
-def run_reference_arm(args, ps, ws, rank):
+def run_reference_arm(args, ws, rank):
+    """The reference's own CPU implementation of the path (oracle/_ref
+    integrate_generic, all host threads) on a bounded sample of the same
+    workload.  Loads only oracle/ -- never the product library."""
     if rank != 0:
         return 0
-    import paper_1310_1191_b200 as pb  # host-side mesh generator only (no GPU use)
-
-    E = 2 * NX * NY * args.nz
-    n_probe = min(E, 200_000)
-    mesh = pb.generate_box_mesh(NX, NY, args.nz * ws, DISTORTION, SEED, first=0, count=n_probe)
-    coeffs = (pb.generate_cdr_coefficients(COEFF_SEED, 0, n_probe) if args.coeff == "cdr"
-              else pb.generate_materials(0, n_probe) if args.coeff == "elasticity" else None)
-    budget = 6.0  # seconds of CPU work per step
-    rates, desc, cores, kind = cpu_reference_rates(ps, args.coeff, budget, mesh, coeffs)
     sys.path.insert(0, str(ROOT / "tests"))
-    from oracle_lib import Reference, laplace_tensor
+    from oracle_lib import REF_SO, Oracle, Reference, cdr_coefficients, materials
 
-    ref = Reference()
+    W = Workload(args, ws, 0)
+    ps = W.ps
+    n_probe = min(W.E, 200_000)
+    gen = Reference() if REF_SO.exists() else Oracle()
+    mesh = gen.box_mesh(*W.mesh, DISTORTION, SEED)[:n_probe].copy()   # rank 0's range starts at 0
+    coeffs = (cdr_coefficients(COEFF_SEED, 0, n_probe) if args.coeff == "cdr"
+              else materials(0, n_probe) if args.coeff == "elasticity" else None)
+    mode = FORMS[args.coeff]
+    budget = 6.0  # seconds of CPU work per step
+    rates, _, cores, kind = cpu_reference_rates(ps, args.coeff, budget, mesh, coeffs)
     n_p = {p: min(len(mesh), max(1, int(rates[p] * budget / len(ps)))) for p in ps}
 
     def one_step(acc):
         for p in ps:
-            c = laplace_tensor() if args.coeff == "laplace" else coeffs[: n_p[p]]
             t0 = time.perf_counter()
-            if args.coeff == "elasticity":
-                ref.integrate_optimized_batch(p, mesh[: n_p[p]], c, threads=cores)
-            else:
-                _, err = ref.integrate_batch(p, mesh[: n_p[p]], c, threads=cores)
-                assert err is None
+            checker(p, mode, mesh[: n_p[p]], None if coeffs is None else coeffs[: n_p[p]], threads=cores)
             acc[p] += time.perf_counter() - t0
 
     scratch = {p: 0.0 for p in ps}
     for _ in range(args.warmup):
         one_step(scratch)
     tsum = {p: 0.0 for p in ps}
+    t0 = time.perf_counter()
     for _ in range(args.steps):
         one_step(tsum)
+    wall = time.perf_counter() - t0
     # Per-element cost depends only on p (SPEC.md:306): the bounded sample's
-    # rate is the rate of the full E-element step.
+    # rate is the rate of the full step of E elements at every p.
     per_p_rate = {p: n_p[p] * args.steps / tsum[p] for p in ps}
     value = step_rate(per_p_rate, ps)
+    sample = (f"each step integrates the first {n_p} elements (per p) of rank 0's range; ms_per_step is that "
+              f"sampled step's measured wall time")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * len(ps) * E / value,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (generate_box_mesh 128x64x64, distortion 0.1, seed 42)",
-        "config": {"workload": f"{args.coeff} p={','.join(map(str, ps))}, {E} prisms per GPU",
-                   "elements_per_gpu": E, "p": ps, "coeff": args.coeff},
-        "per_p": {str(p): {"elements_per_s": per_p_rate[p], "sample_elements": n_p[p]} for p in ps},
-        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": kind,
-                         "sample": f"per step, p-wise first elements: {n_p}"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": W.data(), "config": W.config(),
+        "per_p": {str(p): {"elements_per_s": per_p_rate[p], "sample_elements_per_step": n_p[p]} for p in ps},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": kind, "sample": sample,
+                         "reference_path": checker_name(mode)},
         "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ our arm
-def main():
-    args = parse()
-    ps = [int(x) for x in args.p.split(",")]
-    ws, rank, local = dist_env()
-    if args.impl == "reference":
-        return run_reference_arm(args, ps, ws, rank)
+class Runner:
+    """One rank's device state: inputs resident in HBM, one reused output ring."""
 
+    def __init__(self, args, W, torch, pb, dev, dev_idx, ranks_per_dev):
+        self.args, self.W, self.torch, self.pb, self.dev = args, W, torch, pb, dev
+        E = W.E
+        self.geom_host = pb.generate_box_mesh(*W.mesh, DISTORTION, SEED, first=W.first, count=E, soa=True)
+        self.geom = torch.from_numpy(self.geom_host).to(dev)
+        self.coeff_host, self.coeff = {}, {}
+        self.esz = 4 if args.precision == "f32" else 8
+        self.budget = int(args.out_gb / ranks_per_dev * 1e9 / self.esz)
+        self.out = None
+        self.ctxs = {}
+        self.dev_idx = dev_idx
+        # a dedicated stream: a NULL handle would mean "the context's own stream"
+        self.stream = torch.cuda.Stream(dev)
+        self.sptr = self.stream.cuda_stream
+
+    def coeffs(self, form):
+        pb, torch = self.pb, self.torch
+        if form == "laplace":
+            return None, None
+        if form not in self.coeff:
+            if form == "cdr":
+                h = pb.generate_cdr_coefficients(COEFF_SEED, self.W.first, self.W.E, soa=True)
+            else:
+                h = pb.generate_materials(self.W.first, self.W.E, soa=True)
+            self.coeff_host[form] = h
+            self.coeff[form] = torch.from_numpy(h).to(self.dev)
+        return self.coeff_host[form], self.coeff[form]
+
+    def ctx(self, p, form):
+        n_eq = 3 if form == "elasticity" else 1
+        if (p, n_eq) not in self.ctxs:
+            self.ctxs[(p, n_eq)] = self.pb.Integrator(p, device=self.dev_idx, n_eq=n_eq)
+        return self.ctxs[(p, n_eq)]
+
+    def kk(self, p, form):
+        n_eq = 3 if form == "elasticity" else 1
+        return (n_eq * self.pb.shape_count(p)) ** 2
+
+    def chunk(self, p, form):
+        return min(self.W.E, max(1, self.budget // self.kk(p, form)))
+
+    def ensure_out(self, need):
+        torch = self.torch
+        if self.out is None or self.out.numel() < need:
+            self.out = None
+            torch.cuda.empty_cache()
+            self.out = torch.empty(need, dtype=torch.float32 if self.esz == 4 else torch.float64, device=self.dev)
+
+    def launch(self, p, form, lo, n, out_ptr=None):
+        _, cdev = self.coeffs(form)
+        c0 = None if cdev is None else cdev.data_ptr() + 8 * lo
+        self.ctx(p, form).integrate_device(
+            n, self.geom.data_ptr() + 8 * lo, out_ptr if out_ptr is not None else self.out.data_ptr(),
+            FORMS[form], c0, element_id_base=self.W.first + lo, geom_ld=self.W.E, coeff_ld=self.W.E,
+            stream=self.sptr, precision=self.args.precision)
+
+    def one_pass(self, p, form, on_chunk=None):
+        """Every element of the rank at degree p, chunk by chunk through the output ring."""
+        E, ch = self.W.E, self.chunk(p, form)
+        n_launch = 0
+        for lo in range(0, E, ch):
+            n = min(ch, E - lo)
+            self.launch(p, form, lo, n)
+            n_launch += 1
+            if on_chunk is not None:
+                on_chunk(lo, n)
+        return n_launch
+
+    def samples(self, p, form, local_idx):
+        """Integrate every element (chunked) and copy out the sampled elements' K."""
+        torch, kk = self.torch, self.kk(p, form)
+        got = {}
+
+        def grab(lo, n):
+            sel = [i for i in local_idx if lo <= i < lo + n]
+            if not sel:
+                return
+            self.stream.synchronize()
+            for i in sel:
+                got[i] = self.out[(i - lo) * kk:(i - lo + 1) * kk].double().cpu().numpy()
+
+        self.ensure_out(self.chunk(p, form) * kk)
+        self.one_pass(p, form, grab)
+        self.stream.synchronize()
+        return np.stack([got[i] for i in local_idx]) if local_idx else np.zeros((0, kk))
+
+    def alone(self, p, form, local_idx):
+        """Each sampled element re-integrated as its own 1-element batch (another
+        placement: other CTA, other chunk) -- must be bitwise equal."""
+        torch, kk = self.torch, self.kk(p, form)
+        buf = torch.empty(max(1, len(local_idx)) * kk, dtype=self.out.dtype, device=self.dev)
+        for k, i in enumerate(local_idx):
+            self.launch(p, form, i, 1, out_ptr=buf.data_ptr() + self.esz * k * kk)
+        self.stream.synchronize()
+        return buf[: len(local_idx) * kk].double().cpu().numpy().reshape(len(local_idx), kk)
+
+    def close(self):
+        for c in self.ctxs.values():
+            c.close()
+
+
+def main_ours(args, ws, rank, local):
     import torch
     import paper_1310_1191_b200 as pb
 
-    torch.cuda.set_device(local)
+    ndev = max(1, torch.cuda.device_count())
+    dev_idx = local % ndev
+    shared = ws > ndev  # several ranks on one GPU (test runs on a 1-GPU box): gloo for the reductions
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if shared else dev
 
-    E = 2 * NX * NY * args.nz
-    first = rank * E
-    n_eq = 3 if args.coeff == "elasticity" else 1
-    mode = {"laplace": pb.LAPLACE, "cdr": pb.PER_ELEMENT, "elasticity": pb.ELASTICITY}[args.coeff]
-    # Synthetic inputs for this rank's contiguous range (host-generated, not timed).
-    geom_host = pb.generate_box_mesh(NX, NY, args.nz * ws, DISTORTION, SEED, first=first, count=E, soa=True)
-    geom = torch.from_numpy(geom_host).to(dev)
-    coeff = None
-    coeff_host = None
-    if mode == pb.PER_ELEMENT:
-        coeff_host = pb.generate_cdr_coefficients(COEFF_SEED, first, E, soa=True)
-    elif mode == pb.ELASTICITY:
-        coeff_host = pb.generate_materials(first, E, soa=True)
-    if coeff_host is not None:
-        coeff = torch.from_numpy(coeff_host).to(dev)
-    dim = {p: n_eq * pb.shape_count(p) for p in ps}
-    kk = {p: dim[p] ** 2 for p in ps}
-    # Output: device resident.  A step whose matrices exceed --out-gb streams
-    # through one reused chunk buffer (the ring of SURVEY 8d: K is produced
-    # and left in HBM chunk by chunk; every element is still integrated).
-    esz = 4 if args.precision == "f32" else 8
-    budget = int(args.out_gb * 1e9 / esz)
-    chunk = {p: min(E, max(1, budget // kk[p])) for p in ps}
-    out = torch.empty(max(chunk[p] * kk[p] for p in ps), dtype=torch.float32 if esz == 4 else torch.float64,
-                      device=dev)
-    ctxs = {p: pb.Integrator(p, device=local, n_eq=n_eq) for p in ps}
-    # A dedicated stream: a NULL handle would mean "the context's own stream"
-    # in the C ABI, so torch's legacy default stream (handle 0) is never used.
-    stream = torch.cuda.Stream(dev)
-    sptr = stream.cuda_stream
-    g0 = geom.data_ptr()
-    c0 = coeff.data_ptr() if coeff is not None else None
+    def reduce_max(vals):
+        if not dist:
+            return [float(v) for v in vals]
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().tolist()
 
-    def launch(p, lo, n):
-        ctxs[p].integrate_device(n, g0 + 8 * lo, out.data_ptr(), mode, None if c0 is None else c0 + 8 * lo,
-                                 element_id_base=first + lo, geom_ld=E, coeff_ld=E, stream=sptr,
-                                 precision=args.precision)
+    def gather(obj):
+        if not dist:
+            return [obj]
+        out = [None] * ws
+        dist.all_gather_object(out, obj)
+        return out
 
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    W = Workload(args, ws, rank)
+    ps, E = W.ps, W.E
+    form = args.coeff
+    mode = FORMS[form]
+    n_eq = W.n_eq
+    ranks_per_dev = max(1, -(-ws // ndev)) if shared else 1
+    R = Runner(args, W, torch, pb, dev, dev_idx, ranks_per_dev)
+    kk = {p: R.kk(p, form) for p in ps}
+    R.ensure_out(max(R.chunk(p, form) * kk[p] for p in ps))
+    stream = R.stream
+
+    # ---------------- headline: timed steps ----------------
     def step(events=None):
+        n = 0
         for p in ps:
             if events is not None:
                 events[p][0].record(stream)
-            for lo in range(0, E, chunk[p]):
-                launch(p, lo, min(chunk[p], E - lo))
+            n += R.one_pass(p, form)
             if events is not None:
                 events[p][1].record(stream)
+        return n
 
     for _ in range(max(3, args.warmup)):
         step()
     for p in ps:
-        ctxs[p].check()
+        R.ctx(p, form).check()
     torch.cuda.synchronize(dev)
 
     ev = [{p: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for p in ps}
           for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clocks:
+    launches = 0
+    with ClockSampler(dev_idx) as clocks:
         t_start.record(stream)
         for k in range(args.steps):
-            step(ev[k])
+            launches += step(ev[k])
         t_end.record(stream)
         torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
+    barrier()
     for p in ps:
-        ctxs[p].check()
+        R.ctx(p, form).check()
     elapsed_ms = t_start.elapsed_time(t_end)
     per_p_ms = {p: float(np.mean([ev[k][p][0].elapsed_time(ev[k][p][1]) for k in range(args.steps)])) for p in ps}
-    if dist:
-        t = torch.tensor([elapsed_ms] + [per_p_ms[p] for p in ps], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t[0])
-        per_p_ms = {p: float(t[1 + i]) for i, p in enumerate(ps)}
+    red = reduce_max([elapsed_ms] + [per_p_ms[p] for p in ps])
+    elapsed_ms, per_p_ms = red[0], {p: red[1 + i] for i, p in enumerate(ps)}
     clk = clocks.summary()
     ms_per_step = elapsed_ms / args.steps
-    value = ws * E * len(ps) / (ms_per_step * 1e-3)
-    launches = sum((E + chunk[p] - 1) // chunk[p] for p in ps)
+    value = W.total * len(ps) / (ms_per_step * 1e-3) if args.scaling == "strong" else ws * E * len(ps) / (ms_per_step * 1e-3)
 
-    # -------- parity spot check of the timed outputs (not timed) --------
-    parity = None
-    if rank == 0:
-        sys.path.insert(0, str(ROOT / "tests"))
-        from oracle_lib import REF_SO, Oracle, Reference, laplace_tensor, rel_frobenius
+    # ---------------- roofline inputs ----------------
+    dmma_tf, dfma_tf = pb.measure_fp64_peak(dev_idx)
+    hbm_peak, hbm_src = peaks_hbm()
 
-        worst = 0.0
-        n_checked = 0
-        for p in ps:
-            lo = (E - 1) - ((E - 1) % chunk[p])  # the last chunk is the one left in the buffer
-            idx = sorted({lo, lo + (E - lo) // 2, E - 1})
-            launch(p, lo, E - lo)
-            torch.cuda.synchronize(dev)
-            got = np.stack([out[(i - lo) * kk[p]:(i - lo + 1) * kk[p]].double().cpu().numpy().reshape(dim[p], dim[p])
-                            for i in idx])
-            mesh_aos = geom_host[:, idx].T.reshape(len(idx), 6, 3)
-            if mode == pb.ELASTICITY:
-                mats = coeff_host[:, idx].T
-                if REF_SO.exists():
-                    ref = Reference().integrate_optimized_batch(p, mesh_aos, mats)
-                else:
-                    o = Oracle()
-                    ref = o.integrate_batch(p, mesh_aos, np.stack([o.elasticity_tensor(*m) for m in mats]), n_eq=3)
-            else:
-                c = laplace_tensor() if mode == pb.LAPLACE else coeff_host[:, idx].T.copy()
-                if REF_SO.exists():
-                    ref, err = Reference().integrate_batch(p, mesh_aos, c, threads=0)
-                else:
-                    ref = Oracle().integrate_batch(p, mesh_aos, c)
-            worst = max(worst, float(rel_frobenius(ref, got, axis=(1, 2)).max()))
-            n_checked += len(idx)
-        parity = {"max_rel_frobenius": worst, "tolerance": 1e-12 if esz == 8 else 5e-5, "elements_checked": n_checked,
-                  "checker": ("reference integrate_optimized" if mode == pb.ELASTICITY else
-                              "reference integrate_generic") + " (oracle/_ref)" if REF_SO.exists() else "oracle port"}
-
-    # -------- roofline (dominant kernel = largest share of the step) --------
-    dmma_tf, dfma_tf = pb.measure_fp64_peak(local)
-    peaks = json.load(open(ROOT / "MEASURED_PEAKS.json")) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    per_p = {}
-    for p in ps:
-        t = per_p_ms[p] * 1e-3
-        f_dense = pb.flops_dense_per_element(p, mode, n_eq)
-        f_exec = ctxs[p].flops_executed_per_element(mode)
-        byts = pb.bytes_per_element(p, mode, n_eq) - (8 - esz) * kk[p]
-        bound_s = max(f_dense * E / (dmma_tf * 1e12), byts * E / (hbm_peak * 1e9))
-        per_p[str(p)] = {
-            "elements_per_s": E / t, "ms": per_p_ms[p], "launches": (E + chunk[p] - 1) // chunk[p],
-            "dense_flop_alg_per_element": f_dense, "executed_flop_per_element": f_exec,
-            "bytes_per_element": byts,
-            "dense_tflops": f_dense * E / t / 1e12, "executed_tflops": f_exec * E / t / 1e12,
-            "hbm_gbs": byts * E / t / 1e9,
-            "roofline_bound_elements_per_s": E / bound_s,
-            "frac_of_dense_roofline": bound_s / t,
-            "frac_executed_fp64": f_exec * E / t / 1e12 / dmma_tf,
-            "frac_hbm": byts * E / t / 1e9 / hbm_peak,
+    def fractions(p, frm, ms):
+        n_eq_f = 3 if frm == "elasticity" else 1
+        t = ms * 1e-3
+        f_dense = pb.flops_dense_per_element(p, FORMS[frm], n_eq_f)
+        f_exec = R.ctx(p, frm).flops_executed_per_element(FORMS[frm])
+        byts = pb.bytes_per_element(p, FORMS[frm], n_eq_f) - (8 - R.esz) * R.kk(p, frm)
+        ex = f_exec * E / t / 1e12
+        hb = byts * E / t / 1e9
+        dense_bound_s = max(f_dense * E / (dmma_tf * 1e12), byts * E / (hbm_peak * 1e9))
+        fe, fh = ex / dmma_tf, hb / hbm_peak
+        return {
+            "elements_per_s": E / t, "ms": ms, "launches": -(-E // R.chunk(p, frm)),
+            "dense_flop_alg_per_element": f_dense, "executed_flop_per_element": f_exec, "bytes_per_element": byts,
+            "executed_tflops": ex, "hbm_gbs": hb, "dense_tflops": f_dense * E / t / 1e12,
+            "frac_executed_fp64": fe, "frac_hbm": hb / hbm_peak,
+            "binding": "fp64" if fe >= fh else "hbm", "frac": max(fe, fh),
+            "dense_roofline_elements_per_s": E / dense_bound_s, "frac_of_dense_roofline": dense_bound_s / t,
         }
+
+    per_p = {str(p): fractions(p, form, per_p_ms[p]) for p in ps}
+
+    # ---------------- parity: SURVEY 8(d) samples + placement + digest ----------------
+    cores = os.cpu_count() or 1
+    chk_threads = max(1, cores // min(ws, cores))
+
+    def parity_for(p, frm):
+        ch_host, _ = R.coeffs(frm)
+        md = FORMS[frm]
+        if args.scaling == "strong":
+            gidx = sample_indices(W.total, sample_count(p))
+        else:
+            gidx = sample_indices(W.total, sample_count(p) * ws)
+        lidx = [g - W.first for g in gidx if W.first <= g < W.first + E]
+        got = R.samples(p, frm, lidx)
+        R.ctx(p, frm).check()
+        alone = R.alone(p, frm, lidx)
+        same = bool(np.array_equal(got.view(np.uint64), alone.view(np.uint64)))
+        digests = {W.first + i: hashlib.sha256(got[k].tobytes()).hexdigest() for k, i in enumerate(lidx)}
+        worst = 0.0
+        if lidx:
+            sys.path.insert(0, str(ROOT / "tests"))
+            from oracle_lib import rel_frobenius
+            geoms = np.ascontiguousarray(R.geom_host[:, lidx].T).reshape(len(lidx), 6, 3)
+            cc = None if ch_host is None else np.ascontiguousarray(ch_host[:, lidx].T)
+            ref = checker(p, md, geoms, cc, threads=chk_threads)
+            dim = int(round(np.sqrt(got.shape[1])))
+            worst = float(rel_frobenius(ref, got.reshape(len(lidx), dim, dim), axis=(1, 2)).max())
+        parts = gather((worst, len(lidx), same, digests))
+        all_d = {}
+        for _, _, _, d in parts:
+            all_d.update(d)
+        combined = hashlib.sha256("".join(all_d[g] for g in sorted(all_d)).encode()).hexdigest()
+        return {"max_rel_frobenius": max(x[0] for x in parts), "elements_checked": sum(x[1] for x in parts),
+                "tolerance": 1e-12 if R.esz == 8 else 5e-5, "placement_bitwise_equal": all(x[2] for x in parts),
+                "sample_digest": combined[:32], "checker": checker_name(md)}
+
+    parity = None
+    if not args.no_parity:
+        per_p_parity = {str(p): parity_for(p, form) for p in ps}
+        parity = {"max_rel_frobenius": max(v["max_rel_frobenius"] for v in per_p_parity.values()),
+                  "tolerance": 1e-12 if R.esz == 8 else 5e-5,
+                  "elements_checked": sum(v["elements_checked"] for v in per_p_parity.values()),
+                  "placement_bitwise_equal": all(v["placement_bitwise_equal"] for v in per_p_parity.values()),
+                  "samples": "sample_indices per p: 256 (p<=4), 64 (p=5), 16 (p>=6), SURVEY 8(d)",
+                  "checker": checker_name(mode), "per_p": per_p_parity}
+
+    # ---------------- sweep: p = 1..7, Laplace and CDR ----------------
+    sweep = {}
+    sweep_forms = [f for f in args.sweep.split(",") if f]
+    sweep_ps = [int(x) for x in args.sweep_p.split(",") if x]
+    for frm in sweep_forms:
+        for p in sweep_ps:
+            R.ensure_out(R.chunk(p, frm) * R.kk(p, frm))
+            R.one_pass(p, frm)  # warm-up
+            R.ctx(p, frm).check()
+            times = []
+            for _ in range(max(1, args.reps)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                barrier()
+                torch.cuda.synchronize(dev)
+                a.record(stream)
+                R.one_pass(p, frm)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                times.append(a.elapsed_time(b))
+            R.ctx(p, frm).check()
+            ms = reduce_max([float(np.median(times))])[0]
+            entry = fractions(p, frm, ms)
+            entry["elements_per_s"] = (W.total if args.scaling == "strong" else ws * E) / (ms * 1e-3)
+            entry["reps"] = len(times)
+            if not args.no_parity:
+                entry["parity"] = parity_for(p, frm)
+            sweep[f"{frm}/p{p}"] = entry
+
     dom = max(ps, key=lambda p: per_p_ms[p])
     d = per_p[str(dom)]
-    # DRAM bytes per launch of the dominant kernel: per-element bytes from the
-    # committed ncu capture (profiles/traffic.json, dram__bytes_read+write)
-    # scaled to this launch's element count.
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            per_el = json.load(open(tf)).get(f"p{dom}_{args.coeff}")
-            traffic = per_el * chunk[dom] if per_el is not None else None
+            per_el = json.load(open(tf)).get(f"p{dom}_{form}")
+            traffic = per_el * R.chunk(dom, form) if per_el is not None else None
         except Exception:
             traffic = None
-    kname = ("p1_thread_kernel" if dom == 1 else "p2_lane_kernel") if (dom <= 2 and n_eq == 1) else \
-        f"sumfact_kernel<{dom}, n_eq={n_eq}> (FP64 DMMA)"
+    ctx_dom = R.ctx(dom, form)
+    kname = {(1, 1): "p1_thread_kernel", (2, 1): "p2_lane_kernel", (1, 3): "p1_elastic_lane_kernel",
+             (2, 3): "p2_elastic_warp_kernel", (3, 3): "p3_elastic_cta_kernel"}.get(
+        (dom, n_eq), f"sumfact_kernel<{dom}, n_eq={n_eq}> (FP64 DMMA)")
+    fp64_binds = d["binding"] == "fp64"
     roofline = {
-        "bound": "tensor" if not (dom <= 2 and n_eq == 1) else "fp64", "kernel": kname,
-        "achieved": d["dense_tflops"], "peak": dmma_tf, "unit": "TFLOP/s", "frac": d["dense_tflops"] / dmma_tf,
-        "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write, profiles/traffic.json)",
-        "algorithmic_bytes": d["bytes_per_element"] * chunk[dom],
-        "achieved_note": "SURVEY 8(d) dense FLOP_alg per element x elements / kernel time; the kernels "
-                         "execute fewer FLOPs (sum factorisation, structural zeros, symmetry), so frac can exceed 1",
-        "executed_tflops": d["executed_tflops"], "executed_frac": d["executed_tflops"] / dmma_tf,
-        "hbm_gbs": d["hbm_gbs"], "hbm_peak_gbs": hbm_peak, "hbm_frac": d["hbm_gbs"] / hbm_peak,
-        "peak_source": f"FP64 DMMA m8n8k4 peak measured in-run (DFMA {dfma_tf:.1f} TF/s); "
-                       f"HBM from MEASURED_PEAKS.json" + ("" if peaks else " (absent: B200_PROFILING fallback)"),
+        "bound": "tensor" if fp64_binds else "hbm", "kernel": kname,
+        "achieved": d["executed_tflops"] if fp64_binds else d["hbm_gbs"],
+        "peak": dmma_tf if fp64_binds else hbm_peak,
+        "unit": "TFLOP/s" if fp64_binds else "GB/s",
+        "frac": d["frac"],
+        "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
+        "algorithmic_bytes": d["bytes_per_element"] * R.chunk(dom, form),
+        "note": ("binding-resource fraction: FLOPs the kernel executes (the analytical count of "
+                 "pi_flops_executed_per_element, checked against ncu pipe counters) per launch / launch time, "
+                 "against the FP64 pipe peak measured in-run (DMMA m8n8k4; DMMA and DFMA share one FP64 pipe), "
+                 "or HBM bytes against the measured copy bandwidth -- whichever is the larger fraction"),
+        "fp64": {"executed_tflops": d["executed_tflops"], "peak_tflops": dmma_tf, "frac": d["frac_executed_fp64"],
+                 "peak_source": f"DMMA m8n8k4 measured in-run (DFMA {dfma_tf:.1f} TF/s)"},
+        "hbm": {"gbs": d["hbm_gbs"], "peak_gbs": hbm_peak, "frac": d["frac_hbm"], "peak_source": hbm_src},
+        "dense_count": {"tflops": d["dense_tflops"], "frac_of_fp64_peak": d["dense_tflops"] / dmma_tf,
+                        "note": "SURVEY 8(d) dense FLOP_alg (no symmetry / sum-factorisation credit); the kernels "
+                                "execute fewer FLOPs, so this ratio exceeds 1 and is not a utilisation"},
+        "executed_flop_per_element": ctx_dom.flops_executed_per_element(mode),
     }
 
-    # -------- end to end through the host-buffer C-ABI call --------
+    # ---------------- end to end through the host-buffer C-ABI call ----------------
     e2e = None
-    if not args.no_e2e and esz == 8:
-        geom_aos = torch.from_numpy(np.ascontiguousarray(geom_host.T)).pin_memory()
-        coeff_aos = torch.from_numpy(np.ascontiguousarray(coeff_host.T)).pin_memory() if coeff_host is not None else None
-        # pinned host output: <= 16 GB per rank (8 ranks on one box must not pin
-        # hundreds of GB); every element's K still crosses PCIe into it
+    if not args.no_e2e and R.esz == 8:
+        ch_host, _ = R.coeffs(form)
+        geom_aos = torch.from_numpy(np.ascontiguousarray(R.geom_host.T)).pin_memory()
+        coeff_aos = torch.from_numpy(np.ascontiguousarray(ch_host.T)).pin_memory() if ch_host is not None else None
+        # pinned host output: <= 16 GB per rank; every element's K still crosses PCIe into it
         host_n = {p: min(E, max(1, int(16e9 / 8) // kk[p])) for p in ps}
         host_out = torch.empty(max(host_n[p] * kk[p] for p in ps), dtype=torch.float64).pin_memory()
         ga = geom_aos.numpy()
@@ -419,67 +687,91 @@ def main():
 
         def e2e_step():
             for p in ps:
-                it = ctxs[p]
+                it = R.ctx(p, form)
                 for lo in range(0, E, host_n[p]):
                     n = min(host_n[p], E - lo)
-                    o = host_out[: n * kk[p]].numpy().reshape(n, dim[p], dim[p])
+                    o = host_out[: n * kk[p]].numpy().reshape(n, R.ctx(p, form).dim, R.ctx(p, form).dim)
                     it.integrate_host(ga[lo:lo + n], mode, None if ca is None else ca[lo:lo + n],
-                                      element_id_base=first + lo, out=o)
+                                      element_id_base=W.first + lo, out=o)
 
         for _ in range(max(1, min(args.warmup, 2))):
             e2e_step()
-        if dist:
-            dist.barrier()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             e2e_step()
-        dt = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([dt], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t[0])
-        cw = 0 if coeff_host is None else coeff_host.shape[0]
+        dt = reduce_max([time.perf_counter() - t0])[0]
+        cw = 0 if ch_host is None else ch_host.shape[0]
         h2d = E * 18 * 8 * len(ps) + E * cw * 8 * len(ps)
         d2h = sum(E * kk[p] * 8 for p in ps)
-        e2e = {"value": ws * E * len(ps) * args.steps / dt, "unit": "elements/s",
+        n_all = W.total if args.scaling == "strong" else ws * E
+        e2e = {"value": n_all * len(ps) * args.steps / dt, "unit": "elements/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "pcie_gbs": (h2d + d2h) * args.steps / dt / 1e9,
                "path": "pi_integrate_host (pinned host AoS geometry in, pinned host canonical K out, "
                        "chunked H2D/kernel/D2H on two streams)"}
 
-    # -------- CPU baseline (rank 0, N = 1) --------
+    # ---------------- CPU baseline (rank 0, N = 1) ----------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
+        ch_host, _ = R.coeffs(form)
         n_probe = min(E, 100_000)
-        mesh_aos = np.ascontiguousarray(geom_host[:, :n_probe].T).reshape(n_probe, 6, 3)
-        caos = np.ascontiguousarray(coeff_host[:, :n_probe].T) if coeff_host is not None else None
-        rates, desc, cores, kind = cpu_reference_rates(ps, args.coeff, args.cpu_seconds, mesh_aos, caos)
-        cpu = {"value": step_rate(rates, ps), "unit": "elements/s", "cores": cores, "kind": kind,
-               "sample": desc, "per_p": {str(p): rates[p] for p in ps},
-               "reference_path": "integrate_optimized" if mode == pb.ELASTICITY else "integrate_generic"}
+        mesh_aos = np.ascontiguousarray(R.geom_host[:, :n_probe].T).reshape(n_probe, 6, 3)
+        caos = np.ascontiguousarray(ch_host[:, :n_probe].T) if ch_host is not None else None
+        rates, samples, cores_used, kind = cpu_reference_rates(ps, form, args.cpu_seconds, mesh_aos, caos)
+        rates1, samples1, _, _ = cpu_reference_rates(ps, form, args.cpu1_seconds, mesh_aos, caos, threads=1)
+        cpu = {"value": step_rate(rates, ps), "unit": "elements/s", "cores": cores_used, "kind": kind,
+               "sample": ", ".join(f"p={p}: first {samples[p]} elements" for p in ps) + f" of the same mesh, "
+                         f"{cores_used} threads",
+               "per_p": {str(p): rates[p] for p in ps},
+               "one_core": {"value": step_rate(rates1, ps), "per_p": {str(p): rates1[p] for p in ps},
+                            "sample": ", ".join(f"p={p}: first {samples1[p]} elements" for p in ps)},
+               "reference_path": checker_name(mode)}
+
+    if args.csv and rank == 0:
+        write_csv(args.csv, per_p, sweep, form, E)
 
     if rank == 0:
-        form = {"laplace": "Laplace c=I", "cdr": "seeded per-element CDR tensors",
-                "elasticity": "n_eq=3 isotropic elasticity, per-element (E, nu)"}[args.coeff]
         line = {
             "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if esz == 8 else "f64 compute, f32 K",
-            "data": f"synthetic (generate_box_mesh 128x64x(64*N), distortion 0.1, seed 42; {form})",
-            "config": {"workload": f"{args.coeff} p={','.join(map(str, ps))}, {E} prisms per GPU"
-                                   + (" (BASELINE configs[1])" if args.coeff == "laplace" and ps == [2, 3, 4] else ""),
-                       "elements_per_gpu": E, "p": ps, "coeff": args.coeff, "n_eq": n_eq, "precision": args.precision,
-                       "parallelism": f"element-range x{ws}",
-                       "chunk_elements": {str(p): chunk[p] for p in ps},
-                       "l2": "inputs (151 MB geometry) and outputs (GBs) exceed the 126 MB L2"},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if R.esz == 8 else "f64 compute, f32 K",
+            "data": W.data(), "config": W.config(),
+            "chunk_elements": {str(p): R.chunk(p, form) for p in ps},
             "per_p": per_p, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * launches, "clocks": clk, "parity": parity,
+            "gpu_launches": launches, "clocks": clk, "parity": parity, "sweep": sweep,
+            "ranks_share_gpu": shared,
         }
         print(json.dumps(line), flush=True)
-    for c in ctxs.values():
-        c.close()
+    R.close()
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def write_csv(path, per_p, sweep, form, E):
+    """Rows in the reference's bench CSV schema (bench.cpp:136-141); `kernel_s`
+    is the event-timed device time of one pass over the rank's elements."""
+    cols = ("variant,p,device,elements,input_prep_s,buffer_init_s,kernel_s,output_convert_s,total_s,flops,"
+            "throughput_gflops,input_jac_bytes,input_nojac_bytes,output_bytes")
+    rows = [cols]
+    items = [(f"b200-{form}", int(p), v) for p, v in per_p.items()]
+    items += [(f"b200-{k.split('/')[0]}", int(k.split('/p')[1]), v) for k, v in sweep.items()]
+    for var, p, v in items:
+        ks = v["ms"] * 1e-3
+        flops = v["dense_flop_alg_per_element"] * E
+        out_b = int(round((v["bytes_per_element"] - 144) * E))
+        rows.append(f"{var},{p},\"NVIDIA B200\",{E},0,0,{ks},0,{ks},{int(flops)},{flops / ks / 1e9},"
+                    f"{144 * E},0,{out_b}")
+    Path(path).write_text("\n".join(rows) + "\n")
+
+
+def main(argv=None):
+    args = parse(argv)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference_arm(args, ws, rank)
+    return main_ours(args, ws, rank, local)
 
 
 if __name__ == "__main__":

@@ -262,3 +262,56 @@ def laplace_tensor():
     for d in range(1, 4):
         c[0, 0, d, d] = 1.0
     return c
+
+
+def _mix64(z):
+    """splitmix64 finaliser on uint64 arrays (wrapping arithmetic)."""
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def cdr_coefficients(seed: int, first: int, count: int) -> np.ndarray:
+    """numpy restatement of the synthetic per-element CDR tensors of SURVEY.md
+    8(d) config 3 (the generator behind pi_generate_cdr_coefficients): element
+    g draws 10 counter-based uniforms (splitmix64 of key + 16 g + i), D = R
+    diag(lambda) R^T with lambda in U[0.5, 2] and R a uniform rotation (unit
+    quaternion), convection b in U[-1, 1]^3 at [0][1..3], reaction r in U[0, 1]
+    at [0][0].  AoS [count][16].  Used by bench.py's reference arm so that arm
+    never loads the product library; equal to the product's generator to
+    rounding (tests/test_host.py)."""
+    key = _mix64(np.array([seed ^ 0x43445231], dtype=np.uint64))[0]
+    g = np.arange(first, first + count, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = _mix64(key + g[:, None] * np.uint64(16) + np.arange(10, dtype=np.uint64)[None, :])
+    u = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    lam = 0.5 + 1.5 * u[:, 0:3]
+    r1, r2 = np.sqrt(1.0 - u[:, 3]), np.sqrt(u[:, 3])
+    t1, t2 = 2.0 * np.pi * u[:, 4], 2.0 * np.pi * u[:, 5]
+    qx, qy, qz, qw = r1 * np.sin(t1), r1 * np.cos(t1), r2 * np.sin(t2), r2 * np.cos(t2)
+    R = np.empty((count, 3, 3))
+    R[:, 0, 0] = 1 - 2 * (qy * qy + qz * qz)
+    R[:, 0, 1] = 2 * (qx * qy - qz * qw)
+    R[:, 0, 2] = 2 * (qx * qz + qy * qw)
+    R[:, 1, 0] = 2 * (qx * qy + qz * qw)
+    R[:, 1, 1] = 1 - 2 * (qx * qx + qz * qz)
+    R[:, 1, 2] = 2 * (qy * qz - qx * qw)
+    R[:, 2, 0] = 2 * (qx * qz - qy * qw)
+    R[:, 2, 1] = 2 * (qy * qz + qx * qw)
+    R[:, 2, 2] = 1 - 2 * (qx * qx + qy * qy)
+    c = np.zeros((count, 4, 4))
+    c[:, 1:, 1:] = np.einsum("eik,ek,ejk->eij", R, lam, R)
+    c[:, 0, 1:] = 2.0 * u[:, 6:9] - 1.0
+    c[:, 0, 0] = u[:, 9]
+    return c.reshape(count, 16)
+
+
+def materials(first: int, count: int) -> np.ndarray:
+    """Synthetic per-element (young_E, poisson_nu), AoS [count][2]: the same
+    pure function of the global id as paper_1310_1191_b200.generate_materials."""
+    g = np.arange(first, first + count, dtype=np.uint64)
+    u = ((g * np.uint64(2654435761)) % np.uint64(1000003)).astype(np.float64) / 1000003.0
+    v = ((g * np.uint64(40503) + np.uint64(17)) % np.uint64(999983)).astype(np.float64) / 999983.0
+    return np.ascontiguousarray(np.stack([1.0 + u, 0.2 + 0.15 * v]).T)

@@ -106,6 +106,17 @@ def test_cdr_coefficients_range_independent_and_physical():
     assert not np.array_equal(pb.generate_cdr_coefficients(43, 0, 10), full[:10])
 
 
+def test_checker_side_generators_equal_product():
+    """bench.py's reference arm draws its CDR tensors and materials from the
+    numpy restatements in tests/oracle_lib.py (it must not load the product
+    library): they must give the product generator's values."""
+    from oracle_lib import cdr_coefficients, materials
+
+    for first, count in ((0, 257), (1048000, 1000), (16777000, 216)):
+        assert np.array_equal(cdr_coefficients(42, first, count), pb.generate_cdr_coefficients(42, first, count))
+        assert np.array_equal(materials(first, count), pb.generate_materials(first, count))
+
+
 def test_flop_and_byte_models():
     # SURVEY.md 8(d) table
     want_lap = {1: 3390, 2: 48402, 3: 531408, 4: 2910080, 5: 14934750, 6: 54773565, 7: 170459184}
