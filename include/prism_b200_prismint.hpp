@@ -108,9 +108,13 @@ class Context {
     if (n_eq_ != 3) throw prismint::ConfigError("prism_b200: elasticity needs an n_eq = 3 context");
     if (mats.empty() || (mats.size() != 1 && mats.size() != mesh.size()))
       throw prismint::ConfigError("prism_b200: need one material or one per element");
-    for (const auto& m : mats)
-      if (m.poisson_nu == 0.5)  // lame_parameters, coefficients.cpp:24-27
+    for (const auto& m : mats) {  // lame_parameters' checks, coefficients.cpp:23-32
+      if (m.young_E <= 0.0) throw prismint::DomainError("material: Young modulus must be positive");
+      if (m.poisson_nu <= -1.0 || m.poisson_nu > 0.5)
+        throw prismint::DomainError("material: Poisson ratio must lie in (-1, 0.5]");
+      if (m.poisson_nu == 0.5)
         throw prismint::DomainError("material: nu = 0.5 (incompressible) has no finite Lame lambda");
+    }
     std::vector<double> mbuf(2 * mats.size());
     for (std::size_t k = 0; k < mats.size(); ++k) {
       mbuf[2 * k] = mats[k].young_E;

@@ -330,6 +330,7 @@ class Integrator:
     def __init__(self, p, device=0, n_eq=1, points=None, weights=None, shape_table=None, variant=VARIANT_AUTO):
         L = library()
         self.p = p
+        self.device = device
         self.n_eq = n_eq
         self.n_shape = shape_count(p)
         self.n_q = quadrature_point_count(p)
@@ -382,6 +383,27 @@ class Integrator:
     def flops_executed_per_element(self, coeff_mode=LAPLACE):
         return library().pi_flops_executed_per_element(self._h, coeff_mode)
 
+    def _check_tensor(self, name, t, min_numel, dtypes=("torch.float64",), rows=None, min_cols=None):
+        """Contract checks for a torch tensor handed to the C ABI (kernels.cpp:423-462
+        style ContractViolation); raw integer addresses are the caller's responsibility."""
+        if t is None or isinstance(t, int) or not hasattr(t, "is_cuda"):
+            return
+        if str(t.dtype) not in dtypes:
+            raise ContractViolation(f"{name}: dtype {t.dtype}, expected {' or '.join(dtypes)}")
+        if not t.is_cuda or (t.device.index is not None and t.device.index != self.device):
+            raise ContractViolation(f"{name}: must live on cuda:{self.device} (got {t.device})")
+        if not t.is_contiguous():
+            raise ContractViolation(f"{name}: must be contiguous (a SoA [rows][ld] buffer)")
+        if t.numel() < min_numel:
+            raise ContractViolation(f"{name}: {t.numel()} entries, needs at least {min_numel}")
+        if rows is not None and t.dim() == 2 and t.shape[0] != rows:
+            raise ContractViolation(f"{name}: {t.shape[0]} rows, the weak form needs {rows}")
+        if min_cols is not None and t.dim() == 2 and t.shape[1] < min_cols:
+            raise ContractViolation(f"{name}: leading dimension {t.shape[1]} < n_elem {min_cols}")
+
+    def _coeff_width(self, coeff_mode):
+        return {PER_ELEMENT: 16 * self.n_eq * self.n_eq, ELASTICITY: 2}.get(coeff_mode)
+
     # -- device buffers (torch tensors or raw addresses); asynchronous --
     def integrate_device(self, n_elem, geom, out, coeff_mode=LAPLACE, coeff=None, element_id_base=0,
                          geom_ld=None, coeff_ld=None, out_layout=OUT_CANONICAL, ld_out=0, stream=None,
@@ -401,6 +423,15 @@ class Integrator:
             coeff_ld = coeff.shape[1] if hasattr(coeff, "shape") else n_elem
         # float32 output buffer -> the FP32 output variant (pi_integrate_f32)
         f32 = precision == "f32" or (precision is None and str(getattr(out, "dtype", "")) in ("torch.float32", "float32"))
+        if n_elem > 0:
+            self._check_tensor("geometry", geom, 18 * geom_ld, rows=18 if getattr(geom, "dim", lambda: 0)() == 2 else None,
+                               min_cols=n_elem)
+            kk = self.dim * self.dim
+            need = n_elem * kk if out_layout == OUT_CANONICAL else kk * max(ld_out, n_elem)
+            self._check_tensor("out", out, need, dtypes=("torch.float32",) if f32 else ("torch.float64",))
+            if coeff_mode in (PER_ELEMENT, ELASTICITY):
+                self._check_tensor("coefficients", coeff, self._coeff_width(coeff_mode) * (coeff_ld or n_elem),
+                                   rows=self._coeff_width(coeff_mode), min_cols=n_elem)
         fn = library().pi_integrate_f32 if f32 else library().pi_integrate
         st = fn(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode, caddr, coeff_ld or 0,
                 _addr(out), out_layout, ld_out, stream, C.byref(err))
@@ -427,11 +458,19 @@ class Integrator:
         n = len(geoms)
         if out is None:
             out = np.empty((n, self.dim, self.dim))
+        elif out.size < n * self.dim * self.dim or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ContractViolation(f"out: needs a C-contiguous float64 [{n}][{self.dim}][{self.dim}] buffer")
         cbuf = None
         if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
             cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
+            want = 16 * self.n_eq * self.n_eq if coeff_mode == UNIFORM else 2
+            if cbuf.size != want:
+                raise ContractViolation(f"uniform coefficients: {cbuf.size} values, needs {want}")
         elif coeff_mode in (PER_ELEMENT, ELASTICITY):
             cbuf = np.ascontiguousarray(coeff, dtype=np.float64).reshape(n, -1)
+            if cbuf.shape[1] != self._coeff_width(coeff_mode):
+                raise ContractViolation(f"per-element coefficients: width {cbuf.shape[1]}, the weak form needs "
+                                        f"{self._coeff_width(coeff_mode)}")
         err = _ErrInfo()
         st = library().pi_integrate_host(self._h, n, element_id_base, _addr(geoms), coeff_mode, _addr(cbuf),
                                          _addr(out), chunk_elems, C.byref(err))

@@ -26,7 +26,8 @@ struct LaunchArgs {
   float* out32;         // FP32 output variant (out unused): K rounded to float at the store
   int out_layout;
   int64_t ld_out;
-  unsigned long long* bad;  // min offending global element id (atomicMin)
+  unsigned long long* bad;      // min offending global element id (atomicMin): inverted element
+  unsigned long long* bad_mat;  // ... invalid material (E, nu) of an elasticity element
 };
 
 // Jacobian of the multilinear prism map at xi (geometry.cpp:32-58) for the
@@ -221,7 +222,14 @@ __device__ __forceinline__ void elasticity_block(const double cf[3][3], double w
     }
 }
 
-// Lame parameters (lame_parameters, coefficients.cpp:28-37).
+// lame_parameters' domain checks (coefficients.cpp:23-32): E > 0 and
+// -1 < nu < 0.5; a violation flags the element (DomainError on the host).
+__device__ __forceinline__ void check_material(const LaunchArgs& a, int64_t e, double young, double nu) {
+  if (!(young > 0.0) || !(nu > -1.0) || !(nu < 0.5))
+    atomicMin(a.bad_mat, static_cast<unsigned long long>(a.element_id_base + e));
+}
+
+// Lame parameters (lame_parameters, coefficients.cpp:33-36).
 __device__ __forceinline__ void lame(double young, double nu, double& lam, double& mu) {
   mu = young / (2.0 * (1.0 + nu));
   lam = young * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));

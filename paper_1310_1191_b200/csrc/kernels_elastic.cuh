@@ -24,8 +24,12 @@
 namespace pib {
 
 constexpr int kE1NQ = 6, kE1NSH = 6, kE1DIM = 18, kE1KK = kE1DIM * kE1DIM;
-__constant__ double c_phi_e1[kE1NQ * 4 * kE1NSH];  // tabulate_shapes order [q][k][dof]
-__constant__ double c_pts_e1[kE1NQ * 4];           // xi1, xi2, xi3, w
+// The context's rule and shape table, passed with every launch (kernel
+// parameter space: no shared __constant__ symbol between contexts).
+struct E1Tables {
+  double phi[kE1NQ * 4 * kE1NSH];  // tabulate_shapes order [q][k][dof]
+  double pts[kE1NQ * 4];           // xi1, xi2, xi3, w
+};
 
 constexpr int kE1Warps = 3;
 constexpr int kE1Pitch = kE1KK + 2;  // 16-byte multiple: staged elements leave by TMA bulk stores
@@ -118,7 +122,8 @@ __device__ __forceinline__ void e1_store(T* st, int64_t ld, const double* acc) {
     default: CALL(2); break; \
   }
 
-__global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_kernel(LaunchArgs args) {
+__global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_kernel(const __grid_constant__ LaunchArgs args,
+                                                                           const __grid_constant__ E1Tables tb) {
   using BP = BasisPattern<1>;
   constexpr int NACC = 57;
   extern __shared__ __align__(16) double e1_smem[];
@@ -143,6 +148,7 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
     } else if (warp == 1) {
       const double young = args.coeff ? args.coeff[ec] : args.cu[0];
       const double nu = args.coeff ? args.coeff[args.coeff_ld + ec] : args.cu[1];
+      if (live) check_material(args, e, young, nu);
       lame(young, nu, sMat[lane], sMat[32 + lane]);
     }
     __syncthreads();
@@ -152,11 +158,11 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
 #pragma unroll
       for (int q = warp; q < kE1NQ; q += kE1Warps) {
         double cf[3][3];
-        const double det = jacobian_cofactors<32>(sD + lane, c_pts_e1[4 * q], c_pts_e1[4 * q + 1],
-                                                  c_pts_e1[4 * q + 2], cf);
+        const double det = jacobian_cofactors<32>(sD + lane, tb.pts[4 * q], tb.pts[4 * q + 1],
+                                                  tb.pts[4 * q + 2], cf);
         inverted |= !(det > 0.0);
-        const double id = __drcp_rn(det), dw = det * c_pts_e1[4 * q + 3];
-        const double* ph = c_phi_e1 + q * 4 * kE1NSH;
+        const double id = __drcp_rn(det), dw = det * tb.pts[4 * q + 3];
+        const double* ph = tb.phi + q * 4 * kE1NSH;
         double* gq = sG + q * kE1NG * 32 + lane;
 #pragma unroll
         for (int i = 0; i < kE1NSH; ++i)
@@ -246,9 +252,10 @@ namespace pib {
 // staged in the warp's shared memory (mirrors included) and leaves with
 // coalesced 16-byte stores.
 constexpr int kE2NQ = 18, kE2NSH = 18, kE2DIM = 54, kE2KK = kE2DIM * kE2DIM, kE2NBLK = 171;
-__constant__ double c_phi_e2[kE2NQ * 4 * kE2NSH];  // tabulate_shapes order [q][k][dof]
-__constant__ double c_pts_e2[kE2NQ * 4];           // xi1, xi2, xi3, w
-__constant__ unsigned char c_blk_e2[2 * 192];      // (i, j) of upper-triangle block b (padded)
+struct E2Tables {
+  double phi[kE2NQ * 4 * kE2NSH];  // tabulate_shapes order [q][k][dof]
+  double pts[kE2NQ * 4];           // xi1, xi2, xi3, w
+};
 
 constexpr int kE2Warps = 4;
 constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
@@ -257,23 +264,27 @@ constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases 
 constexpr int kE2Phi = kE2NQ * 4 * kE2NSH;          // the shape table, staged per CTA
 constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
 
-__global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(LaunchArgs args) {
+__global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const __grid_constant__ LaunchArgs args,
+                                                                  const __grid_constant__ E2Tables tb) {
   using BP = BasisPattern<2>;
   extern __shared__ __align__(16) double e2_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sw = e2_smem + warp * (kE2WarpDoubles + 2);  // this warp's region (16-byte aligned)
   // lanes read the table at different points: shared memory, not the constant bank
   double* sPhi = e2_smem + (kE2WarpDoubles + 2) * kE2Warps;
-  for (int i = threadIdx.x; i < kE2Phi; i += 32 * kE2Warps) sPhi[i] = c_phi_e2[i];
+  for (int i = threadIdx.x; i < kE2Phi; i += 32 * kE2Warps) sPhi[i] = tb.phi[i];
   __syncthreads();
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kE2Warps;
   // the lane's blocks (i, j)
   int bi[kE2BPL], bj[kE2BPL];
 #pragma unroll
   for (int k = 0; k < kE2BPL; ++k) {
-    const int b = lane + 32 * k;
-    bi[k] = c_blk_e2[2 * b];
-    bj[k] = c_blk_e2[2 * b + 1];
+    // upper-triangle block b = (i, j >= i) in row-major order (padding: b >= 171)
+    int b = lane + 32 * k, i = 0;
+    if (b >= kE2NBLK) b = kE2NBLK - 1;
+    while (b >= kE2NSH - i) b -= kE2NSH - i++;
+    bi[k] = i;
+    bj[k] = i + b;
   }
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kE2Warps + warp; e < args.n_elem; e += nwarps) {
     // ---- geometry, material, then per-point gradients (lane = point) ----
@@ -281,6 +292,7 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
     {
       const double young = args.coeff ? args.coeff[e] : args.cu[0];
       const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+      if (threadIdx.x % 32 == 0) check_material(args, e, young, nu);
       lame(young, nu, lam, mu);
     }
     double x[18], d[21];
@@ -291,9 +303,9 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(Launc
     if (lane < kE2NQ) {
       const int q = lane;
       double cf[3][3];
-      const double det = jacobian_cofactors(d, c_pts_e2[4 * q], c_pts_e2[4 * q + 1], c_pts_e2[4 * q + 2], cf);
+      const double det = jacobian_cofactors(d, tb.pts[4 * q], tb.pts[4 * q + 1], tb.pts[4 * q + 2], cf);
       inverted = !(det > 0.0);
-      const double id = __drcp_rn(det), dw = det * c_pts_e2[4 * q + 3];
+      const double id = __drcp_rn(det), dw = det * tb.pts[4 * q + 3];
       double* gq = sw + q * (kE2NSH * 3 + 2);
 #pragma unroll
       for (int i = 0; i < kE2NSH; ++i)
@@ -429,6 +441,7 @@ __global__ void __launch_bounds__(kE3Threads, 2) p3_elastic_cta_kernel(LaunchArg
     {
       const double young = args.coeff ? args.coeff[e] : args.cu[0];
       const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+      if (threadIdx.x % 32 == 0) check_material(args, e, young, nu);
       lame(young, nu, lam, mu);
     }
     // (1) inverse Jacobian and dw per point (threads 0..47)

@@ -27,20 +27,25 @@
 namespace pib {
 
 constexpr int kP2NQ = 18, kP2NSH = 18, kP2KK = kP2NSH * kP2NSH;
-__constant__ double c_phi_p2[kP2NQ * 4 * kP2NSH];  // tabulate_shapes order [q][k][dof]
-__constant__ double c_pts_p2[kP2NQ * 4];           // xi1, xi2, xi3, w
-__constant__ float c_phi_p2f[kP2NQ * 4 * kP2NSH];   // the same table in FP32 (FP32 arithmetic variant)
+// The context's rule and shape table travel with every launch as a kernel
+// parameter (constant bank 0, warp-uniform reads like __constant__), so
+// contexts with different tables never race on a shared symbol.
+struct P2Tables {
+  double phi[kP2NQ * 4 * kP2NSH];  // tabulate_shapes order [q][k][dof]
+  double pts[kP2NQ * 4];           // xi1, xi2, xi3, w
+  float phif[kP2NQ * 4 * kP2NSH];  // the same table in FP32 (FP32 arithmetic variant)
+};
 
 // Compute type T: double (the 1e-12 path) or float (FP32 variant, bound 5e-5).
 template <typename T>
-__device__ __forceinline__ const T* p2_phi();
+__device__ __forceinline__ const T* p2_phi(const P2Tables& tb);
 template <>
-__device__ __forceinline__ const double* p2_phi<double>() {
-  return c_phi_p2;
+__device__ __forceinline__ const double* p2_phi<double>(const P2Tables& tb) {
+  return tb.phi;
 }
 template <>
-__device__ __forceinline__ const float* p2_phi<float>() {
-  return c_phi_p2f;
+__device__ __forceinline__ const float* p2_phi<float>(const P2Tables& tb) {
+  return tb.phif;
 }
 
 // staged element pitch: 16-byte multiple (TMA bulk stores of whole elements),
@@ -95,13 +100,13 @@ __device__ __forceinline__ constexpr int p2_row(int r) {
 
 // The warp's rows over all rule points.
 template <typename T, bool GENERAL, bool SYM, int W>
-__device__ __forceinline__ void p2_rows(const T* __restrict__ sM, int lane, T* acc) {
+__device__ __forceinline__ void p2_rows(const P2Tables& tb, const T* __restrict__ sM, int lane, T* acc) {
   using BP = BasisPattern<2>;
   using C = P2Cfg<GENERAL, SYM>;
   constexpr int K0 = GENERAL ? 0 : 1, NR = C::NR, NM = C::NM;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
-    const T* ph = p2_phi<T>() + q * 4 * kP2NSH;
+    const T* ph = p2_phi<T>(tb) + q * 4 * kP2NSH;
     const T* mq = sM + q * NM * 32 + lane;
     // G_l(i) = sum_k phi_k(i) M_kl, M read one row k at a time (only the
     // rows k the warp's basis functions do not annihilate)
@@ -151,11 +156,11 @@ __device__ __forceinline__ void p2_rows(const T* __restrict__ sM, int lane, T* a
 // formed densely from the warp-uniform phi_k(i), the column loop skips the
 // structural zeros of phi_l(j) at compile time.
 template <typename T>
-__device__ __forceinline__ void p2_row_general(const T* __restrict__ sM, int lane, int i, T* acc) {
+__device__ __forceinline__ void p2_row_general(const P2Tables& tb, const T* __restrict__ sM, int lane, int i, T* acc) {
   using BP = BasisPattern<2>;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
-    const T* ph = p2_phi<T>() + q * 4 * kP2NSH;
+    const T* ph = p2_phi<T>(tb) + q * 4 * kP2NSH;
     const T* mq = sM + q * 16 * 32 + lane;
     T g[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
@@ -227,7 +232,8 @@ __device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, 
   }
 
 template <bool GENERAL, bool SYM, typename T = double>
-__global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(LaunchArgs args) {
+__global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const __grid_constant__ LaunchArgs args,
+                                                                         const __grid_constant__ P2Tables tb) {
   using C = P2Cfg<GENERAL, SYM>;
   constexpr int NR = C::NR;
   extern __shared__ __align__(16) double p2_smem[];
@@ -284,8 +290,8 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
 #pragma unroll
       for (int q = warp; q < kP2NQ; q += C::NW) {
         double M[16];
-        const double det = point_block<GENERAL, 32, 32>(sD + lane, c_pts_p2[4 * q], c_pts_p2[4 * q + 1],
-                                                        c_pts_p2[4 * q + 2], c_pts_p2[4 * q + 3], sC + lane, M);
+        const double det = point_block<GENERAL, 32, 32>(sD + lane, tb.pts[4 * q], tb.pts[4 * q + 1],
+                                                        tb.pts[4 * q + 2], tb.pts[4 * q + 3], sC + lane, M);
         inverted |= !(det > 0.0);
         if (GENERAL) {
 #pragma unroll
@@ -303,11 +309,11 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(Launch
 #pragma unroll
     for (int i = 0; i < C::NACC; ++i) acc[i] = T(0);
     if constexpr (SYM) {
-#define P2_ACC(W) p2_rows<T, GENERAL, SYM, W>(sM, lane, acc)
+#define P2_ACC(W) p2_rows<T, GENERAL, SYM, W>(tb, sM, lane, acc)
       P2_WARP_SWITCH(P2_ACC)
 #undef P2_ACC
     } else {
-      p2_row_general(sM, lane, warp, acc);
+      p2_row_general(tb, sM, lane, warp, acc);
     }
     __syncthreads();  // M no longer read: the buffer becomes the output staging
     if (args.out_layout == PI_OUT_SOA) {

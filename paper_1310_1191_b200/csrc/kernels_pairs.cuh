@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
         if (ptid == 0) {
           const double young = args.coeff ? args.coeff[e] : args.cu[0];
           const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+          check_material(args, e, young, nu);
           lame(young, nu, sC[0], sC[1]);
         }
       }

@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
           const int64_t ec = e < args.n_elem ? e : args.n_elem - 1;
           const double young = args.coeff ? args.coeff[ec] : args.cu[0];
           const double nu = args.coeff ? args.coeff[args.coeff_ld + ec] : args.cu[1];
+          if (e < args.n_elem && (w % C::NITEM) == 0) check_material(args, e, young, nu);
           lame(young, nu, sC[2 * ptid], sC[2 * ptid + 1]);
         }
       }

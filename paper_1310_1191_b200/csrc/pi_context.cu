@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -23,6 +24,13 @@ struct CallRecord {
   int64_t ld, base, n;
 };
 
+// Completion of the context's work on one caller stream (pi_check waits on
+// these events instead of the whole device).
+struct StreamMark {
+  cudaStream_t stream;
+  cudaEvent_t done;
+};
+
 struct pi_context {
   int device = 0, p = 0, n_eq = 1, n_q = 0, n_shape = 0;
   int variant = PI_VARIANT_AUTO;
@@ -34,13 +42,18 @@ struct pi_context {
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
   int p2_ctas_f[3] = {0, 0, 0};  // ... and per FP32-arithmetic instantiation
-  std::vector<float> h_phi_f;    // p = 2 shape table in FP32
+  // per-context rule / shape tables of the p <= 2 register kernels, passed by
+  // value with every launch (kernel parameter space)
+  std::unique_ptr<P2Tables> p2tab;
+  std::unique_ptr<E1Tables> e1tab;
+  std::unique_ptr<E2Tables> e2tab;
   int e1_ctas = 0;             // persistent grid of p1_elastic_lane_kernel
   int e2_ctas = 0;             // persistent grid of p2_elastic_warp_kernel
   int e3_ctas = 0;             // persistent grid of p3_elastic_cta_kernel
   double* d_pts4 = nullptr; // rule as [n_q][xi1, xi2, xi3, w]
-  unsigned long long* d_bad = nullptr;
+  unsigned long long* d_bad = nullptr;  // [0] lowest inverted element id, [1] lowest invalid material id
   std::vector<CallRecord> calls;
+  std::vector<StreamMark> marks;
   // host streaming path
   cudaStream_t hs[2] = {nullptr, nullptr};
   double* hbuf = nullptr;
@@ -50,8 +63,30 @@ struct pi_context {
 namespace {
 
 pi_status cuda_fail(pi_error_info* err, cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) {
+    // out of device memory is a capacity problem of the request, not a CUDA
+    // failure (CapacityError, errors.hpp:16); the error is not sticky
+    cudaGetLastError();
+    if (err) err->cuda_error = static_cast<int>(e);
+    return set_error(err, PI_E_CAPACITY, "%s: device memory exhausted", what);
+  }
   if (err) err->cuda_error = static_cast<int>(e);
   return set_error(err, PI_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// lame_parameters' checks (coefficients.cpp:23-32).
+pi_status check_material_host(double young, double nu, int64_t element, pi_error_info* err) {
+  const char* why = nullptr;
+  if (!(young > 0.0))
+    why = "material: Young modulus must be positive";
+  else if (!(nu > -1.0) || nu > 0.5)
+    why = "material: Poisson ratio must lie in (-1, 0.5]";
+  else if (nu == 0.5)
+    why = "material: nu = 0.5 (incompressible) has no finite Lame lambda";
+  if (!why) return PI_OK;
+  pi_status st = set_error(err, PI_E_DOMAIN, "%s (element %lld)", why, (long long)element);
+  if (err) err->element = element;
+  return st;
 }
 
 #define PI_CUDA(call, what)                                   \
@@ -75,6 +110,26 @@ pi_status upload(T** dst, const std::vector<T>& src, pi_error_info* err) {
   cudaError_t e = cudaMalloc(dst, std::max<size_t>(sizeof(T), src.size() * sizeof(T)));
   if (e == cudaSuccess && !src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
   return e == cudaSuccess ? PI_OK : cuda_fail(err, e, "upload per-p tables");
+}
+
+// Records the completion of the context's latest work on stream s.
+pi_status mark_stream(pi_context* ctx, cudaStream_t s, pi_error_info* err) {
+  if (s == ctx->stream) return PI_OK;  // pi_check synchronises the context's own stream directly
+  for (auto& m : ctx->marks)
+    if (m.stream == s) {
+      PI_CUDA(cudaEventRecord(m.done, s), "record completion");
+      return PI_OK;
+    }
+  if (ctx->marks.size() >= 64) {  // bound the table: wait for the oldest stream and forget it
+    PI_CUDA(cudaEventSynchronize(ctx->marks.front().done), "completion wait");
+    cudaEventDestroy(ctx->marks.front().done);
+    ctx->marks.erase(ctx->marks.begin());
+  }
+  StreamMark m{s, nullptr};
+  PI_CUDA(cudaEventCreateWithFlags(&m.done, cudaEventDisableTiming), "completion event");
+  PI_CUDA(cudaEventRecord(m.done, s), "record completion");
+  ctx->marks.push_back(m);
+  return PI_OK;
 }
 
 int resolve_variant(const pi_context* ctx) {
@@ -146,9 +201,9 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
     wpad.resize((wpad.size() + 1) / 2 * 2, 0.0);
     if ((st = upload(&ctx->d_w, wpad, err)) != PI_OK) return fail(st);
   }
-  ce = cudaMalloc(&ctx->d_bad, sizeof(unsigned long long));
+  ce = cudaMalloc(&ctx->d_bad, 2 * sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMalloc"));
-  ce = cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long));
+  ce = cudaMemset(ctx->d_bad, 0xff, 2 * sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
 
   // The kernels skip the basis' structural zeros (BasisPattern): the table
@@ -180,6 +235,26 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
     }
   }
+  if (p == 2 && n_eq == 1) {
+    ctx->p2tab = std::make_unique<P2Tables>();
+    std::memcpy(ctx->p2tab->phi, ctx->h_phi.data(), sizeof(ctx->p2tab->phi));
+    for (int i = 0; i < kP2NQ * 4 * kP2NSH; ++i) ctx->p2tab->phif[i] = static_cast<float>(ctx->h_phi[i]);
+  }
+  if (p == 2 && n_eq == 3) {
+    ctx->e2tab = std::make_unique<E2Tables>();
+    std::memcpy(ctx->e2tab->phi, ctx->h_phi.data(), sizeof(ctx->e2tab->phi));
+  }
+  if (p == 1 && n_eq == 3) {
+    ctx->e1tab = std::make_unique<E1Tables>();
+    std::memcpy(ctx->e1tab->phi, ctx->h_phi.data(), sizeof(ctx->e1tab->phi));
+  }
+  for (int q = 0; q < nq && p <= 2; ++q)
+    for (int c = 0; c < 4; ++c) {
+      const double v = c < 3 ? ctx->h_pts[3 * q + c] : ctx->h_w[q];
+      if (ctx->p2tab) ctx->p2tab->pts[4 * q + c] = v;
+      if (ctx->e2tab) ctx->e2tab->pts[4 * q + c] = v;
+      if (ctx->e1tab) ctx->e1tab->pts[4 * q + c] = v;
+    }
   if (p == 3 && n_eq == 3) {
     cudaFuncSetAttribute(p3_elastic_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(E3Smem::BYTES));
@@ -240,7 +315,6 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
     ctx->p2_ctas_f[0] = ctas(p2_lane_kernel<false, true, float>, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES);
     ctx->p2_ctas_f[1] = ctas(p2_lane_kernel<true, true, float>, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES);
     ctx->p2_ctas_f[2] = ctas(p2_lane_kernel<true, false, float>, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES);
-    ctx->h_phi_f.assign(ctx->h_phi.begin(), ctx->h_phi.end());
     ctx->p2_ok = true;
   }
   ce = cudaGetLastError();
@@ -264,6 +338,7 @@ pi_status pi_context_destroy(pi_context* ctx) {
   cudaFree(ctx->d_tri);
   cudaFree(ctx->d_bad);
   cudaFree(ctx->d_pts4);
+  for (auto& m : ctx->marks) cudaEventDestroy(m.done);
   if (ctx->hbuf) cudaFree(ctx->hbuf);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -316,6 +391,7 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   a.out_layout = out_layout;
   a.ld_out = ld_out;
   a.bad = ctx->d_bad;
+  a.bad_mat = ctx->d_bad + 1;
   const int ne = ctx->n_eq, ncoef = 16 * ne * ne;
   bool general = false, symmetric = true;
   int form = kFormLaplace;
@@ -352,8 +428,8 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
         a.coeff = coeff;
         a.coeff_ld = coeff_ld;
       } else {
-        if (coeff[1] == 0.5)  // lame_parameters, coefficients.cpp:24-27
-          return set_error(err, PI_E_DOMAIN, "material: nu = 0.5 (incompressible) has no finite Lame lambda");
+        const pi_status ms = check_material_host(coeff[0], coeff[1], -1, err);
+        if (ms != PI_OK) return ms;
         a.cu[0] = coeff[0];
         a.cu[1] = coeff[1];
       }
@@ -373,62 +449,33 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_elem, ctx->e3_ctas));
     p3_elastic_cta_kernel<<<grid, kE3Threads, E3Smem::BYTES, s>>>(a, t);
   } else if (e2_warp) {
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e2, ctx->d_phi, sizeof(double) * kE2NQ * 4 * kE2NSH, 0,
-                                    cudaMemcpyDeviceToDevice, s),
-            "upload p=2 shape table");
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_e2, ctx->d_pts4, sizeof(double) * kE2NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
-            "upload p=2 rule");
-    static const std::vector<unsigned char> blk = [] {
-      std::vector<unsigned char> t(2 * 192, 0);
-      int b = 0;
-      for (int i = 0; i < kE2NSH; ++i)
-        for (int j = i; j < kE2NSH; ++j, ++b) {
-          t[2 * b] = static_cast<unsigned char>(i);
-          t[2 * b + 1] = static_cast<unsigned char>(j);
-        }
-      return t;
-    }();
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_blk_e2, blk.data(), blk.size(), 0, cudaMemcpyHostToDevice, s),
-            "upload p=2 block table");
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + kE2Warps - 1) / kE2Warps, ctx->e2_ctas));
-    p2_elastic_warp_kernel<<<grid, 32 * kE2Warps, kE2SmemBytes, s>>>(a);
+    p2_elastic_warp_kernel<<<grid, 32 * kE2Warps, kE2SmemBytes, s>>>(a, *ctx->e2tab);
   } else if (e1_lane) {
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_e1, ctx->d_phi, sizeof(double) * kE1NQ * 4 * kE1NSH, 0,
-                                    cudaMemcpyDeviceToDevice, s),
-            "upload p=1 shape table");
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_e1, ctx->d_pts4, sizeof(double) * kE1NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
-            "upload p=1 rule");
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + 31) / 32, ctx->e1_ctas));
-    p1_elastic_lane_kernel<<<grid, 32 * kE1Warps, E1Smem::BYTES, s>>>(a);
+    p1_elastic_lane_kernel<<<grid, 32 * kE1Warps, E1Smem::BYTES, s>>>(a, *ctx->e1tab);
   } else if (ctx->p == 2 && ne == 1 && v == PI_VARIANT_DENSE) {
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2, ctx->d_phi, sizeof(double) * kP2NQ * 4 * kP2NSH, 0,
-                                    cudaMemcpyDeviceToDevice, s),
-            "upload p=2 shape table");
-    PI_CUDA(cudaMemcpyToSymbolAsync(c_pts_p2, ctx->d_pts4, sizeof(double) * kP2NQ * 4, 0, cudaMemcpyDeviceToDevice, s),
-            "upload p=2 rule");
     const int64_t groups = (n_elem + 31) / 32;
     const int which = !general ? 0 : (symmetric ? 1 : 2);
+    const P2Tables& tb = *ctx->p2tab;
     if (out32) {
       // FP32 output variant: FP32 arithmetic too (the table in FP32, M rounded
       // after the FP64 point block); bound 5e-5
-      PI_CUDA(cudaMemcpyToSymbolAsync(c_phi_p2f, ctx->h_phi_f.data(), sizeof(float) * kP2NQ * 4 * kP2NSH, 0,
-                                      cudaMemcpyHostToDevice, s),
-              "upload p=2 FP32 shape table");
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas_f[which]));
       if (!general)
-        p2_lane_kernel<false, true, float><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<false, true, float><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a, tb);
       else if (symmetric)
-        p2_lane_kernel<true, true, float><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<true, true, float><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a, tb);
       else
-        p2_lane_kernel<true, false, float><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<true, false, float><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a, tb);
     } else {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas[which]));
       if (!general)
-        p2_lane_kernel<false, true><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<false, true><<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES, s>>>(a, tb);
       else if (symmetric)
-        p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<true, true><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a, tb);
       else
-        p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a);
+        p2_lane_kernel<true, false><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a, tb);
     }
   } else if (v == PI_VARIANT_DENSE && ne == 1) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
@@ -446,7 +493,7 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   PI_CUDA(cudaGetLastError(), "kernel launch");
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
   if (ctx->calls.size() > 4096) ctx->calls.erase(ctx->calls.begin(), ctx->calls.begin() + 2048);
-  return PI_OK;
+  return mark_stream(ctx, s, err);
 }
 }  // namespace
 
@@ -488,6 +535,7 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
   a.geom_ld = geom_ld;
   a.out = out;
   a.bad = ctx->d_bad;
+  a.bad_mat = ctx->d_bad + 1;
   DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
@@ -496,35 +544,16 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
                                                                                             ctx->n_shape, f, f_const);
   PI_CUDA(cudaGetLastError(), "load-vector launch");
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
-  return PI_OK;
+  return mark_stream(ctx, s, err);
 }
 
-pi_status pi_check(pi_context* ctx, pi_error_info* err) {
-  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
-  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
-  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  PI_CUDA(cudaStreamSynchronize(ctx->stream), "stream synchronize");
-  PI_CUDA(cudaDeviceSynchronize(), "device synchronize");
-  unsigned long long bad = ~0ull;
-  PI_CUDA(cudaMemcpy(&bad, ctx->d_bad, sizeof bad, cudaMemcpyDeviceToHost), "read inverted-element flag");
-  if (bad == ~0ull) {
-    ctx->calls.clear();
-    return PI_OK;
-  }
-  PI_CUDA(cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long)), "reset flag");
-  const int64_t gid = static_cast<int64_t>(bad);
-  // Describe it like InvertedElementError (errors.cpp:33-41): first failing
-  // rule point in rule order, with its determinant.
+namespace {
+// Describes an inverted element like InvertedElementError (errors.cpp:33-41):
+// the first failing rule point in rule order and its determinant.  g: AoS
+// [6][3] geometry of the element, or NULL when it is no longer available.
+pi_status report_inverted(pi_context* ctx, int64_t gid, const double* g, pi_error_info* err) {
   double xi[3] = {0, 0, 0}, det = 0.0;
-  for (auto it = ctx->calls.rbegin(); it != ctx->calls.rend(); ++it) {
-    if (gid < it->base || gid >= it->base + it->n) continue;
-    const int64_t le = gid - it->base;
-    double g[18];
-    bool got = true;
-    for (int c = 0; c < 18; ++c)
-      if (cudaMemcpy(&g[c], it->geom + c * it->ld + le, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
-        got = false;
-    if (!got) break;
+  if (g)
     for (int q = 0; q < ctx->n_q; ++q) {
       double inv[9], d;
       if (!jacobian_terms(g, &ctx->h_pts[3 * q], d, inv)) {
@@ -533,9 +562,6 @@ pi_status pi_check(pi_context* ctx, pi_error_info* err) {
         break;
       }
     }
-    break;
-  }
-  ctx->calls.clear();
   pi_status st = set_error(err, PI_E_INVERTED_ELEMENT, "inverted element %lld: det=%f at xi=(%f, %f, %f)",
                            (long long)gid, det, xi[0], xi[1], xi[2]);
   if (err) {
@@ -546,6 +572,60 @@ pi_status pi_check(pi_context* ctx, pi_error_info* err) {
   return st;
 }
 
+// Waits for every stream the context launched on since the last check (its
+// own stream and the recorded caller streams -- never the whole device),
+// then reads and resets the error flags.  Returns the flags through bad[2].
+pi_status drain(pi_context* ctx, unsigned long long bad[2], pi_error_info* err) {
+  bad[0] = bad[1] = ~0ull;
+  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  PI_CUDA(cudaStreamSynchronize(ctx->stream), "stream synchronize");
+  for (auto& m : ctx->marks) PI_CUDA(cudaEventSynchronize(m.done), "stream synchronize");
+  for (auto& h : ctx->hs)
+    if (h) PI_CUDA(cudaStreamSynchronize(h), "stream synchronize");
+  PI_CUDA(cudaMemcpy(bad, ctx->d_bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "read error flags");
+  if (bad[0] != ~0ull || bad[1] != ~0ull)
+    PI_CUDA(cudaMemset(ctx->d_bad, 0xff, 2 * sizeof(unsigned long long)), "reset error flags");
+  return PI_OK;
+}
+
+pi_status material_error(int64_t gid, pi_error_info* err) {
+  pi_status st = set_error(err, PI_E_DOMAIN,
+                           "material of element %lld: lame_parameters needs E > 0 and -1 < nu < 0.5", (long long)gid);
+  if (err) err->element = gid;
+  return st;
+}
+}  // namespace
+
+pi_status pi_check(pi_context* ctx, pi_error_info* err) {
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  unsigned long long bad[2];
+  const pi_status ds = drain(ctx, bad, err);
+  if (ds != PI_OK) return ds;
+  if (bad[1] != ~0ull) {
+    ctx->calls.clear();
+    return material_error(static_cast<int64_t>(bad[1]), err);
+  }
+  if (bad[0] == ~0ull) {
+    ctx->calls.clear();
+    return PI_OK;
+  }
+  const int64_t gid = static_cast<int64_t>(bad[0]);
+  double g[18];
+  bool got = false;
+  for (auto it = ctx->calls.rbegin(); it != ctx->calls.rend(); ++it) {
+    if (gid < it->base || gid >= it->base + it->n) continue;
+    const int64_t le = gid - it->base;
+    got = true;
+    for (int c = 0; c < 18; ++c)  // SoA [18][ld] -> AoS [6][3]
+      if (cudaMemcpy(&g[c], it->geom + c * it->ld + le, sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        got = false;
+    break;
+  }
+  ctx->calls.clear();
+  return report_inverted(ctx, gid, got ? g : nullptr, err);
+}
+
 pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
                             int coeff_mode, const double* coeff, double* out, int64_t chunk_elems,
                             pi_error_info* err) {
@@ -553,7 +633,20 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
   if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
   if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
   if (!geom_aos || !out) return set_error(err, PI_E_CONTRACT, "NULL host buffers");
-  PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+  if ((coeff_mode == PI_COEFF_PER_ELEMENT || coeff_mode == PI_COEFF_ELASTICITY) && !coeff)
+    return set_error(err, PI_E_CONTRACT, "per-element coefficient buffer is NULL");
+  // Errors of earlier asynchronous calls on this context surface here first
+  // (the header's contract), so this call's flags are its own.
+  {
+    const pi_status prev = pi_check(ctx, err);
+    if (prev != PI_OK) return prev;
+  }
+  // run_batch validates every material before integrating (lame_parameters)
+  if (coeff_mode == PI_COEFF_ELASTICITY)
+    for (int64_t e = 0; e < n_elem; ++e) {
+      const pi_status ms = check_material_host(coeff[2 * e], coeff[2 * e + 1], element_id_base + e, err);
+      if (ms != PI_OK) return ms;
+    }
   const int64_t dim = static_cast<int64_t>(ctx->n_shape) * ctx->n_eq;
   const int64_t kk = dim * dim;
   // per-element coefficient width: the tensor, or (E, nu) for elasticity
@@ -577,6 +670,18 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
   }
   for (auto& s : ctx->hs)
     if (!s) PI_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create");
+  // Every exit waits for both slots' copies: no DMA into or out of the
+  // caller's host buffers may still be pending when this call returns.
+  auto settle = [&](pi_status st) {
+    cudaStreamSynchronize(ctx->hs[0]);
+    cudaStreamSynchronize(ctx->hs[1]);
+    return st;
+  };
+#define PI_CUDA_SETTLE(call, what)                                       \
+  do {                                                                   \
+    cudaError_t e_ = (call);                                             \
+    if (e_ != cudaSuccess) return settle(cuda_fail(err, e_, what));      \
+  } while (0)
   int64_t done = 0;
   int slot = 0;
   while (done < n_elem) {
@@ -588,53 +693,40 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
     double* d_geom = d_aos + 18 * chunk_elems;
     double* d_caos = d_geom + 18 * chunk_elems;
     double* d_coef = d_caos + cw * chunk_elems;
-    PI_CUDA(cudaMemcpyAsync(d_aos, geom_aos + 18 * done, sizeof(double) * 18 * cnt, cudaMemcpyHostToDevice, s), "H2D geometry");
+    PI_CUDA_SETTLE(cudaMemcpyAsync(d_aos, geom_aos + 18 * done, sizeof(double) * 18 * cnt, cudaMemcpyHostToDevice, s),
+                   "H2D geometry");
     aos_to_soa_kernel<<<static_cast<unsigned>((18 * cnt + 255) / 256), 256, 0, s>>>(d_aos, d_geom, cnt, 18, cnt);
     const double* cptr = coeff;
     int64_t cld = 0;
     if (cw) {
-      PI_CUDA(cudaMemcpyAsync(d_caos, coeff + cw * done, sizeof(double) * cw * cnt, cudaMemcpyHostToDevice, s),
-              "H2D coefficients");
+      PI_CUDA_SETTLE(cudaMemcpyAsync(d_caos, coeff + cw * done, sizeof(double) * cw * cnt, cudaMemcpyHostToDevice, s),
+                     "H2D coefficients");
       aos_to_soa_kernel<<<static_cast<unsigned>((cw * cnt + 255) / 256), 256, 0, s>>>(d_caos, d_coef, cnt, cw, cnt);
       cptr = d_coef;
       cld = cnt;
     }
     pi_status st = pi_integrate(ctx, cnt, element_id_base + done, d_geom, cnt, coeff_mode, cptr, cld, d_out,
                                 PI_OUT_CANONICAL, 0, s, err);
-    if (st != PI_OK) return st;
-    PI_CUDA(cudaMemcpyAsync(out + kk * done, d_out, sizeof(double) * kk * cnt, cudaMemcpyDeviceToHost, s), "D2H K");
+    if (st != PI_OK) return settle(st);
+    PI_CUDA_SETTLE(cudaMemcpyAsync(out + kk * done, d_out, sizeof(double) * kk * cnt, cudaMemcpyDeviceToHost, s),
+                   "D2H K");
     done += cnt;
     slot ^= 1;
   }
-  PI_CUDA(cudaStreamSynchronize(ctx->hs[0]), "sync");
-  PI_CUDA(cudaStreamSynchronize(ctx->hs[1]), "sync");
-  // Device geometry of the streamed chunks is gone; report by element id.
-  unsigned long long bad = ~0ull;
-  PI_CUDA(cudaMemcpy(&bad, ctx->d_bad, sizeof bad, cudaMemcpyDeviceToHost), "read flag");
+#undef PI_CUDA_SETTLE
+  settle(PI_OK);
+  unsigned long long bad[2];
+  const pi_status ds = drain(ctx, bad, err);
   ctx->calls.clear();
-  if (bad != ~0ull) {
-    PI_CUDA(cudaMemset(ctx->d_bad, 0xff, sizeof(unsigned long long)), "reset flag");
-    const int64_t gid = static_cast<int64_t>(bad);
-    const double* g = geom_aos + 18 * (gid - element_id_base);
-    double xi[3] = {0, 0, 0}, det = 0.0;
-    for (int q = 0; q < ctx->n_q; ++q) {
-      double inv[9], d;
-      if (!jacobian_terms(g, &ctx->h_pts[3 * q], d, inv)) {
-        std::memcpy(xi, &ctx->h_pts[3 * q], sizeof xi);
-        det = d;
-        break;
-      }
-    }
-    pi_status st = set_error(err, PI_E_INVERTED_ELEMENT, "inverted element %lld: det=%f at xi=(%f, %f, %f)",
-                             (long long)gid, det, xi[0], xi[1], xi[2]);
-    if (err) {
-      err->element = gid;
-      err->det = det;
-      std::memcpy(err->xi, xi, sizeof xi);
-    }
-    return st;
-  }
-  return PI_OK;
+  if (ds != PI_OK) return ds;
+  if (bad[1] != ~0ull) return material_error(static_cast<int64_t>(bad[1]), err);
+  if (bad[0] == ~0ull) return PI_OK;
+  // Device geometry of the streamed chunks is gone: describe the element from
+  // the caller's host buffer (the flag can only hold this call's ids, the
+  // earlier calls were drained above).
+  const int64_t gid = static_cast<int64_t>(bad[0]);
+  const bool mine = gid >= element_id_base && gid < element_id_base + n_elem;
+  return report_inverted(ctx, gid, mine ? geom_aos + 18 * (gid - element_id_base) : nullptr, err);
 }
 
 pi_status pi_integrate_host_multi(pi_context* const* ctxs, int n_ctx, int64_t n_elem, int64_t element_id_base,

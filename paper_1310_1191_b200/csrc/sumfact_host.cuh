@@ -3,6 +3,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 
 #include "kernels_pairs.cuh"
@@ -10,6 +11,30 @@
 #include "sumfact_api.hpp"
 
 namespace pib {
+
+constexpr int kMaxDevices = 64;
+
+// Persistent grid of a kernel on the current device: SMs x resident CTAs per
+// SM, computed once per (kernel, device) -- a per-device cache that host
+// threads driving different GPUs (pi_integrate_host_multi) share safely.
+template <typename K>
+int persistent_grid(std::atomic<int>* cache, K kernel, int threads, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& slot = cache[dev >= 0 && dev < kMaxDevices ? dev : 0];
+  int c = slot.load(std::memory_order_relaxed);
+  if (c == 0) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    c = std::max(1, std::max(1, sms) * std::max(1, per_sm));
+    slot.store(c, std::memory_order_relaxed);
+  }
+  return c;
+}
 
 template <int P, int NE>
 struct SumFactHost {
@@ -28,16 +53,8 @@ struct SumFactHost {
   // instantiation), each looping over (element group, a'-group, column block) items.
   template <int FORM, bool SYM>
   static int resident_ctas() {
-    static int c = 0;
-    if (c == 0) {
-      int dev = 0, sms = 0, per_sm = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_kernel<P, NE, FORM, SYM>, CK<SYM>::NTHREADS,
-                                                    CK<SYM>::SMEM_BYTES);
-      c = std::max(1, sms * std::max(1, per_sm));
-    }
-    return c;
+    static std::atomic<int> cache[kMaxDevices] = {};
+    return persistent_grid(cache, sumfact_kernel<P, NE, FORM, SYM>, CK<SYM>::NTHREADS, CK<SYM>::SMEM_BYTES);
   }
   // symmetric forms at high p: the pair-split kernel (kernels_pairs.cuh)
   // (measured: faster for scalar forms at p >= 5; slower for n_eq = 3, whose
@@ -56,15 +73,8 @@ struct SumFactHost {
   static bool go_pairs(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
     if constexpr (kPairs) {
       using PC = PairsConfig<P, NE>;
-      static int c = 0;
-      if (c == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sumfact_pairs_kernel<P, NE, FORM>, PC::NTHREADS,
-                                                      PC::SMEM_BYTES);
-        c = std::max(1, sms * std::max(1, per_sm));
-      }
+      static std::atomic<int> cache[kMaxDevices] = {};
+      const int c = persistent_grid(cache, sumfact_pairs_kernel<P, NE, FORM>, PC::NTHREADS, PC::SMEM_BYTES);
       const dim3 grid(static_cast<unsigned>(std::min<int64_t>(a.n_elem, c)));  // element-major CTAs
       sumfact_pairs_kernel<P, NE, FORM><<<grid, PC::NTHREADS, PC::SMEM_BYTES, s>>>(a, t);
       return true;

@@ -44,14 +44,20 @@ def test_golden_cdr_uniform_nonsymmetric(p):
     assert err.max() <= 1e-12, err
 
 
-@pytest.mark.parametrize("p", [2, 4, 6])
+@pytest.mark.parametrize("p", range(1, 8))
 def test_symmetric_uniform_tensor_path(p):
-    """A symmetric anisotropic tensor takes the symmetric (mirrored) path."""
+    """A symmetric anisotropic tensor with value/derivative couplings
+    c[0][k] = c[k][0] != 0 takes the symmetric (mirrored) path of every launch
+    shape, including the w0 terms of the pair-split kernel."""
     rng = np.random.default_rng(p)
     a = rng.normal(size=(3, 3))
     c = np.zeros((4, 4))
     c[1:, 1:] = np.eye(3) + 0.2 * (a + a.T)
     c[0, 0] = 0.7
+    b = 0.3 * rng.normal(size=3)
+    c[0, 1:] = b
+    c[1:, 0] = b
+    assert np.array_equal(c, c.T)
     geoms = pb.generate_box_mesh(3, 2, 2, 0.2, seed=p)
     got = integrate(p, geoms, pb.UNIFORM, c)
     assert np.abs(got - np.transpose(got, (0, 2, 1))).max() <= 1e-13 * np.abs(got).max()
