@@ -90,6 +90,7 @@ def parse(argv=None):
     ap.add_argument("--reps", type=int, default=3, help="timed passes per sweep entry (median reported)")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-load", action="store_true", help="skip the load-vector measurements")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=16.0, help="CPU baseline budget (all threads)")
     ap.add_argument("--cpu1-seconds", type=float, default=4.0, help="CPU baseline budget (1 thread)")
@@ -399,21 +400,26 @@ class Runner:
             torch.cuda.empty_cache()
             self.out = torch.empty(need, dtype=torch.float32 if self.esz == 4 else torch.float64, device=self.dev)
 
-    def launch(self, p, form, lo, n, out_ptr=None):
+    def launch(self, p, form, lo, n, out_ptr=None, load=None):
+        """load: (device F buffer [E][n_shape], device f [E]) -> pi_integrate_load."""
         _, cdev = self.coeffs(form)
         c0 = None if cdev is None else cdev.data_ptr() + 8 * lo
+        kw = {}
+        if load is not None:
+            nsh = self.pb.shape_count(p)
+            kw = {"load_out": load[0].data_ptr() + 8 * nsh * lo, "f": load[1].data_ptr() + 8 * lo}
         self.ctx(p, form).integrate_device(
             n, self.geom.data_ptr() + 8 * lo, out_ptr if out_ptr is not None else self.out.data_ptr(),
             FORMS[form], c0, element_id_base=self.W.first + lo, geom_ld=self.W.E, coeff_ld=self.W.E,
-            stream=self.sptr, precision=self.args.precision)
+            stream=self.sptr, precision=self.args.precision, **kw)
 
-    def one_pass(self, p, form, on_chunk=None):
+    def one_pass(self, p, form, on_chunk=None, load=None):
         """Every element of the rank at degree p, chunk by chunk through the output ring."""
         E, ch = self.W.E, self.chunk(p, form)
         n_launch = 0
         for lo in range(0, E, ch):
             n = min(ch, E - lo)
-            self.launch(p, form, lo, n)
+            self.launch(p, form, lo, n, load=load)
             n_launch += 1
             if on_chunk is not None:
                 on_chunk(lo, n)
@@ -637,6 +643,56 @@ def main_ours(args, ws, rank, local):
                 entry["parity"] = parity_for(p, frm)
             sweep[f"{frm}/p{p}"] = entry
 
+    # ---------------- load vectors: fused into the stiffness pass vs standalone ----------------
+    loadv = None
+    if not args.no_load and n_eq == 1 and R.esz == 8:
+        loadv = {}
+        fvals = torch.linspace(0.5, 2.0, E, dtype=torch.float64, device=dev)
+
+        def timed(fn):
+            fn()
+            times = []
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize(dev)
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                times.append(a.elapsed_time(b))
+            return reduce_max([float(np.median(times))])[0]
+
+        for p in ps:
+            nsh = pb.shape_count(p)
+            fbuf = torch.empty(E * nsh, dtype=torch.float64, device=dev)
+            R.ensure_out(R.chunk(p, form) * R.kk(p, form))
+            ms_fused = timed(lambda: R.one_pass(p, form, load=(fbuf, fvals)))
+            it = R.ctx(p, form)
+            ms_alone = timed(lambda: it.load_vectors_device(E, R.geom, fbuf, f=fvals, stream=R.sptr))
+            it.check()
+            entry = {"fused_elements_per_s": ws * E / (ms_fused * 1e-3), "fused_ms": ms_fused,
+                     "stiffness_only_ms": per_p_ms[p], "fusion_overhead": ms_fused / per_p_ms[p] - 1.0,
+                     "standalone_elements_per_s": ws * E / (ms_alone * 1e-3), "standalone_ms": ms_alone,
+                     "standalone_hbm_gbs": (144 + 8 + 8 * nsh) * E / (ms_alone * 1e-3) / 1e9}
+            if not args.no_parity:
+                # F = f * column 0 of the c[0][0][0][0] = 1 mass matrix (the reference's integrate_generic)
+                lidx = sample_indices(E, 64)
+                R.one_pass(p, form, load=(fbuf, fvals))
+                torch.cuda.synchronize(dev)
+                got = fbuf.view(E, nsh)[lidx].cpu().numpy()
+                sys.path.insert(0, str(ROOT / "tests"))
+                from oracle_lib import rel_frobenius
+                geoms = np.ascontiguousarray(R.geom_host[:, lidx].T).reshape(len(lidx), 6, 3)
+                cm = np.zeros((len(lidx), 16))
+                cm[:, 0] = 1.0
+                mass = checker(p, FORMS["cdr"], geoms, cm, threads=chk_threads)
+                ref = mass[:, :, 0] * fvals[lidx].cpu().numpy()[:, None]
+                entry["parity"] = {"max_rel_frobenius": float(rel_frobenius(ref, got, axis=1).max()),
+                                   "tolerance": 1e-12, "elements_checked": len(lidx),
+                                   "checker": "f x column 0 of the reference integrate_generic mass matrix"}
+            loadv[str(p)] = entry
+            del fbuf
+
     dom = max(ps, key=lambda p: per_p_ms[p])
     d = per_p[str(dom)]
     traffic = None
@@ -739,7 +795,7 @@ def main_ours(args, ws, rank, local):
             "data": W.data(), "config": W.config(),
             "chunk_elements": {str(p): R.chunk(p, form) for p in ps},
             "per_p": per_p, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk, "parity": parity, "sweep": sweep,
+            "gpu_launches": launches, "clocks": clk, "parity": parity, "sweep": sweep, "load_vectors": loadv,
             "ranks_share_gpu": shared,
         }
         print(json.dumps(line), flush=True)

@@ -144,6 +144,17 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
                           const double* geom, int64_t geom_ld, const double* f, double f_const,
                           double* out, void* stream, pi_error_info* err);
 
+/* pi_integrate with the load vectors fused into the same pass (scalar weak
+ * forms, n_eq = 1, FP64): besides K, writes F_i = sum_q det*w_q * f * phi_i(x_q)
+ * to load_out (device [n_elem][n_shape]) from the Jacobians the stiffness
+ * kernel already forms -- no second read of the geometry.  f / f_const as in
+ * pi_load_vectors.  Same bound as pi_load_vectors: F equals f times column 0
+ * of the c[0][0][0][0] = 1 mass matrix of integrate_generic. */
+pi_status pi_integrate_load(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                            int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
+                            int out_layout, int64_t ld_out, const double* f, double f_const, double* load_out,
+                            void* stream, pi_error_info* err);
+
 /* Waits for the context's outstanding work and reports inverted elements
  * (PI_E_INVERTED_ELEMENT with element/det/xi filled) or CUDA errors. */
 pi_status pi_check(pi_context* ctx, pi_error_info* err);

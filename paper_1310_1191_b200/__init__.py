@@ -139,6 +139,8 @@ def library():
     L.pi_integrate.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, C.c_int,
                                C.c_int64, vp, E]
     L.pi_integrate_f32.argtypes = L.pi_integrate.argtypes
+    L.pi_integrate_load.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, C.c_int,
+                                    C.c_int64, vp, C.c_double, vp, vp, E]
     L.pi_integrate_host_multi.argtypes = [C.POINTER(vp), C.c_int, C.c_int64, C.c_int64, vp, C.c_int, vp, vp,
                                           C.c_int64, E]
     L.pi_load_vectors.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_double, vp, vp, E]
@@ -407,9 +409,11 @@ class Integrator:
     # -- device buffers (torch tensors or raw addresses); asynchronous --
     def integrate_device(self, n_elem, geom, out, coeff_mode=LAPLACE, coeff=None, element_id_base=0,
                          geom_ld=None, coeff_ld=None, out_layout=OUT_CANONICAL, ld_out=0, stream=None,
-                         precision=None):
+                         precision=None, load_out=None, f=None, f_const=1.0):
         """pi_integrate on device memory.  geom: SoA [18][geom_ld]; out: device buffer
-        (float64; float32 selects the FP32 output variant, or precision="f32" for raw addresses)."""
+        (float64; float32 selects the FP32 output variant, or precision="f32" for raw addresses).
+        load_out (device [n_elem][n_shape] float64): also the load vectors in the same pass
+        (pi_integrate_load; f: device [n_elem] per-element values, else f_const)."""
         err = _ErrInfo()
         cbuf = None
         if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
@@ -432,6 +436,17 @@ class Integrator:
             if coeff_mode in (PER_ELEMENT, ELASTICITY):
                 self._check_tensor("coefficients", coeff, self._coeff_width(coeff_mode) * (coeff_ld or n_elem),
                                    rows=self._coeff_width(coeff_mode), min_cols=n_elem)
+        if load_out is not None:
+            if f32:
+                raise ContractViolation("fused load vectors need an FP64 stiffness output")
+            if n_elem > 0:
+                self._check_tensor("load_out", load_out, n_elem * self.n_shape)
+                self._check_tensor("f", f, n_elem)
+            st = library().pi_integrate_load(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode,
+                                             caddr, coeff_ld or 0, _addr(out), out_layout, ld_out, _addr(f),
+                                             float(f_const), _addr(load_out), stream, C.byref(err))
+            _raise(st, err)
+            return
         fn = library().pi_integrate_f32 if f32 else library().pi_integrate
         st = fn(self._h, n_elem, element_id_base, _addr(geom), geom_ld, coeff_mode, caddr, coeff_ld or 0,
                 _addr(out), out_layout, ld_out, stream, C.byref(err))

@@ -28,7 +28,16 @@ struct LaunchArgs {
   int64_t ld_out;
   unsigned long long* bad;      // min offending global element id (atomicMin): inverted element
   unsigned long long* bad_mat;  // ... invalid material (E, nu) of an elasticity element
+  // Fused load vectors (pi_integrate_load, n_eq = 1): when fout != nullptr the
+  // stiffness kernels also write F_i = sum_q det w_q f phi_i(q) as [n_elem][n_shape],
+  // f = fsrc[e] (per element) or fconst.
+  double* fout;
+  const double* fsrc;
+  double fconst;
 };
+
+// f of element e for the fused load vector.
+__device__ __forceinline__ double load_f(const LaunchArgs& a, int64_t e) { return a.fsrc ? a.fsrc[e] : a.fconst; }
 
 // Jacobian of the multilinear prism map at xi (geometry.cpp:32-58) for the
 // SoA/smem vertex array x[v*3+i], its determinant and the cofactor inverse

@@ -56,7 +56,8 @@ struct BasisPattern {
 // per-point block M (kernels_common.cuh); the basis' structural zeros are
 // skipped at compile time (13 of the 24 phi entries per point are non-zero),
 // so the contraction costs about half the dense loop nest's FMAs.
-template <bool GENERAL>
+// LOAD: also the load vector F_i = sum_q det w_q f phi_0(i, q) (6 more accumulators).
+template <bool GENERAL, bool LOAD = false>
 __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : PI_P1_MINB)
     p1_thread_kernel(LaunchArgs args, DenseTables tab) {
   constexpr int kP1Threads = p1_threads<GENERAL>();
@@ -100,6 +101,10 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
   double K[KK];
 #pragma unroll
   for (int i = 0; i < KK; ++i) K[i] = 0.0;
+  double F[LOAD ? NSH : 1];
+  const double fe = LOAD ? load_f(args, ec) : 0.0;
+#pragma unroll
+  for (int i = 0; i < (LOAD ? NSH : 1); ++i) F[i] = 0.0;
   bool inverted = false;
 
 #pragma unroll 1
@@ -108,6 +113,11 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
     const double det = point_block<GENERAL>(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], sW[q], cf, M);
     inverted |= !(det > 0.0);
     const double* ph = sPhi + q * 4 * NSH;
+    if constexpr (LOAD) {
+      const double dwf = det * sW[q] * fe;
+#pragma unroll
+      for (int i = 0; i < NSH; ++i) F[i] = fma(dwf, ph[i], F[i]);
+    }
     constexpr int K0 = GENERAL ? 0 : 1;  // Laplace has no value row
     // G_l(i) = sum_k phi_k(i) M_kl ; K_ij += sum_l G_l(i) phi_l(j)
 #pragma unroll
@@ -138,6 +148,10 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
       for (int j = 0; j < i; ++j) K[i * NSH + j] = K[j * NSH + i];
   }
   if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
+  if (LOAD && live) {
+#pragma unroll
+    for (int i = 0; i < NSH; ++i) args.fout[e * NSH + i] = F[i];
+  }
 
   if (args.out_layout == PI_OUT_SOA) {
     if (live) {
@@ -217,6 +231,69 @@ __global__ void __launch_bounds__(32 * kLoadWarps)
     double s = 0.0;
     for (int q = 0; q < nq; ++q) s += dw[q] * tab.phi[static_cast<int64_t>(q) * 4 * nsh + i];
     args.out[e * nsh + i] = s;
+  }
+}
+
+// Load vectors through the tensor-product structure (p >= 2 with the
+// sum-factorisation tables): phi_0(t*NV + a, (s, z)) = m_t(s) P_a(z), so
+//     F(t,a) = sum_s X_2(t,s) u(s,a),   u(s,a) = sum_z P_a(z) dw(s,z),
+// dw = det w f at every rule point (q = z*NS + s, reference order).  A CTA
+// takes kLoadSfElems elements: edge vectors, dw and u per element in shared
+// memory; F leaves as one contiguous coalesced block per CTA.  Per element
+// the kernel reads 144 B of geometry (+8 B of f) and writes 8 N_sh bytes: an
+// HBM-bound stream (the per-p tables are a few KB and stay in L1).
+struct LoadSfTables {
+  const double* tri;     // xi1 [NS], xi2 [NS]
+  const double* yline;   // (P, P') [NZ][NV] pairs, xi3 [NZ]
+  const double* xplain;  // X as [NSP][3][ntps]; y = 2 is m_t(s)
+  const double* w;       // [NQ] reference order
+  int ns, nz, nv, nt, ntps;
+};
+constexpr int kLoadSfElems = 16, kLoadSfThreads = 256;
+__global__ void __launch_bounds__(kLoadSfThreads)
+    load_vector_sf_kernel(LaunchArgs args, LoadSfTables tb, const double* f, double f_const) {
+  const int ns = tb.ns, nz = tb.nz, nv = tb.nv, nt = tb.nt, nq = ns * nz, nsh = nt * nv;
+  extern __shared__ __align__(16) double sl[];
+  double* sD = sl;                          // [E][21]
+  double* sDW = sD + kLoadSfElems * 21;     // [E][nq]
+  double* sU = sDW + kLoadSfElems * nq;     // [E][ns][nv]
+  const int tid = threadIdx.x;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kLoadSfElems;
+  const int64_t left = args.n_elem - e0;
+  const int ne = left < kLoadSfElems ? static_cast<int>(left) : kLoadSfElems;
+  if (tid < ne) {
+    double x[18], d[21];
+#pragma unroll
+    for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e0 + tid];
+    prism_edges(x, d);
+#pragma unroll
+    for (int c = 0; c < 21; ++c) sD[tid * 21 + c] = d[c];
+  }
+  __syncthreads();
+  for (int i = tid; i < ne * nq; i += kLoadSfThreads) {
+    const int el = i / nq, q = i - el * nq, z = q / ns, s = q - z * ns;
+    double cf[3][3];
+    const double det = jacobian_cofactors(sD + el * 21, __ldg(tb.tri + s), __ldg(tb.tri + ns + s),
+                                          __ldg(tb.yline + 2 * nv * nz + z), cf);
+    if (!(det > 0.0)) flag_inverted(args.bad, args.element_id_base + e0 + el);
+    const double fe = f ? f[e0 + el] : f_const;
+    sDW[el * nq + s * nz + z] = det * __ldg(tb.w + q) * fe;
+  }
+  __syncthreads();
+  for (int i = tid; i < ne * ns * nv; i += kLoadSfThreads) {
+    const int el = i / (ns * nv), r = i - el * ns * nv, s = r / nv, a = r - s * nv;
+    const double* dw = sDW + el * nq + s * nz;
+    double u = 0.0;
+    for (int z = 0; z < nz; ++z) u = fma(__ldg(tb.yline + 2 * (z * nv + a)), dw[z], u);
+    sU[(el * ns + s) * nv + a] = u;
+  }
+  __syncthreads();
+  for (int i = tid; i < ne * nsh; i += kLoadSfThreads) {  // coalesced: consecutive dofs of consecutive elements
+    const int el = i / nsh, dof = i - el * nsh, t = dof / nv, a = dof - t * nv;
+    const double* u = sU + el * ns * nv + a;
+    double acc = 0.0;
+    for (int s = 0; s < ns; ++s) acc = fma(__ldg(tb.xplain + (s * 3 + 2) * tb.ntps + t), u[s * nv], acc);
+    args.out[(e0 + el) * nsh + dof] = acc;
   }
 }
 

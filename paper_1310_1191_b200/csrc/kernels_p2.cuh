@@ -79,6 +79,9 @@ struct P2Cfg {
   static constexpr int OFF_C = OFF_G + 2 * 18 * 32;      // coefficients, double buffered [2][16][32]
   static constexpr int SMEM_DOUBLES = OFF_C + (GENERAL ? 2 * 16 * 32 : 0);
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
+  // fused load vectors: det w f per (point, lane) after the rest
+  static constexpr int OFF_DW = SMEM_DOUBLES;
+  static constexpr size_t SMEM_BYTES_LOAD = (SMEM_DOUBLES + kP2NQ * 32) * sizeof(double);
   // per-SMSP register file (16K regs; warps dealt round-robin to the 4 SMSPs):
   // 9-warp CTAs x3 need <= 72 registers, one 18-warp CTA <= 96
   static constexpr int MAXREG = SYM ? 72 : 96;
@@ -231,7 +234,9 @@ __device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, 
     default: CALL(8); break; \
   }
 
-template <bool GENERAL, bool SYM, typename T = double>
+// LOAD (FP64 only): also the load vector F_i = sum_q det w_q f phi_0(i, q);
+// det w f per point is kept from the M pass, each warp sums its own rows.
+template <bool GENERAL, bool SYM, typename T = double, bool LOAD = false>
 __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const __grid_constant__ LaunchArgs args,
                                                                          const __grid_constant__ P2Tables tb) {
   using C = P2Cfg<GENERAL, SYM>;
@@ -293,6 +298,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
         const double det = point_block<GENERAL, 32, 32>(sD + lane, tb.pts[4 * q], tb.pts[4 * q + 1],
                                                         tb.pts[4 * q + 2], tb.pts[4 * q + 3], sC + lane, M);
         inverted |= !(det > 0.0);
+        if constexpr (LOAD) p2_smem[C::OFF_DW + q * 32 + lane] = det * tb.pts[4 * q + 3] * load_f(args, min(e, args.n_elem - 1));
         if (GENERAL) {
 #pragma unroll
           for (int k = 0; k < 16; ++k) sM[(q * 16 + k) * 32 + lane] = static_cast<T>(M[k]);
@@ -316,6 +322,19 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
       p2_row_general(tb, sM, lane, warp, acc);
     }
     __syncthreads();  // M no longer read: the buffer becomes the output staging
+    if constexpr (LOAD) {
+      static_assert(sizeof(T) == 8, "fused load vectors are FP64");
+      if (live) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int i = r == 0 ? warp : kP2NSH - 1 - warp;
+          double fi = 0.0;
+#pragma unroll
+          for (int q = 0; q < kP2NQ; ++q) fi = fma(p2_smem[C::OFF_DW + q * 32 + lane], tb.phi[q * 4 * kP2NSH + i], fi);
+          args.fout[e * kP2NSH + i] = fi;
+        }
+      }
+    }
     if (args.out_layout == PI_OUT_SOA) {
       if (live) {
         if constexpr (SYM) {

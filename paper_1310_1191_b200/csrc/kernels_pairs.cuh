@@ -78,6 +78,9 @@ struct PairsConfig {
   static constexpr int OFF_W = OFF_TRI + 2 * NS;
   static constexpr int SMEM_DOUBLES = OFF_W + (NQ + 1) / 2 * 2;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
+  // fused load vectors (sumfact_load_vectors): dw [NSP][NZ], u [NSP][NV]
+  static constexpr int OFF_LDW = SMEM_DOUBLES, OFF_LU = OFF_LDW + NSP * NZ;
+  static constexpr size_t SMEM_BYTES_LOAD = sizeof(double) * (OFF_LU + NSP * NV);
   // named barriers: FULL 1..3, EMPTY 4..6, producers 7
   static constexpr int BAR_FULL = 1, BAR_EMPTY = 1 + NBUF, BAR_PROD = 1 + 2 * NBUF;
 };
@@ -187,6 +190,7 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
           const double det = jacobian_cofactors(sGeom, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
           const double w8 = sW[z * NS + s], wd = w8 * __drcp_rn(det);
           if (!(det > 0.0)) flag_inverted(args.bad, args.element_id_base + e);
+          if (NE == 1 && args.fout) smem[C::OFF_LDW + s * NZ + z] = det * w8 * load_f(args, e);
 #pragma unroll
           for (int blk = 0; blk < NE * NE; ++blk) {
             double M[16];
@@ -201,9 +205,15 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
         } else {
 #pragma unroll
           for (int k = 0; k < 16 * NE * NE; ++k) Mi[k * C::MPITCH] = 0.0;
+          if (NE == 1 && args.fout) smem[C::OFF_LDW + s * NZ + z] = 0.0;
         }
       }
       named_sync(C::BAR_PROD, C::NPT);
+      if (NE == 1 && C::MALL && args.fout) {
+        sumfact_load_vectors<NS, C::NSP, NZ, NV, NT, NTPS>(args, e, 1, smem + C::OFF_LDW, smem + C::OFF_LU, sXP, PD,
+                                                         ptid, C::NPT, C::BAR_PROD);
+        named_sync(C::BAR_PROD, C::NPT);
+      }
     };
     for (int64_t it = 0; it < my_items; ++it) {
       const int64_t e = blockIdx.x + (it / C::NITEM) * gridDim.x;

@@ -357,7 +357,42 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR
   static constexpr int STAGE_DOUBLES = BULK ? L::EPC * ESTRIDE : NCW * STAGE_PER_WARP;
   static constexpr int SMEM_DOUBLES = OFF_STAGE + STAGE_DOUBLES;
   static constexpr size_t SMEM_BYTES = sizeof(double) * SMEM_DOUBLES;
+  // fused load vectors (n_eq = 1): det w f per point [EPC][NSP][NZ] and
+  // u(s, a) [EPC][NSP][NV] after the rest; launched with SMEM_BYTES_LOAD
+  static constexpr int OFF_LDW = SMEM_DOUBLES;
+  static constexpr int OFF_LU = OFF_LDW + L::EPC * S::NSP * S::NZ;
+  static constexpr size_t SMEM_BYTES_LOAD = sizeof(double) * (OFF_LU + L::EPC * S::NSP * S::NV);
 };
+
+// Fused load vector of the producers' current elements (pi_integrate_load):
+// phi_0(t*NV + a, (s, z)) = m_t(s) P_a(z) = X_2(t, s) P_a(z), so
+//     F(t, a) = sum_s X_2(t, s) u(s, a),   u(s, a) = sum_z P_a(z) dw(s, z)
+// from dw = det w f per point (sDW [ne][NSP][NZ], zero at padded s); one
+// contiguous coalesced store of N_sh doubles per element.
+template <int NS, int NSP, int NZ, int NV, int NT, int NTPS>
+__device__ __forceinline__ void sumfact_load_vectors(const LaunchArgs& args, int64_t e0, int ne, const double* sDW,
+                                                     double* sU, const double* sXP, const double2* PD, int ptid,
+                                                     int npt, int bar) {
+  for (int i = ptid; i < ne * NSP * NV; i += npt) {
+    const int el = i / (NSP * NV), r = i % (NSP * NV), s = r / NV, a = r % NV;
+    const double* dw = sDW + (el * NSP + s) * NZ;
+    double u = 0.0;
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) u = fma(PD[z * NV + a].x, dw[z], u);
+    sU[i] = u;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(npt) : "memory");
+  constexpr int NSH = NT * NV;
+  for (int i = ptid; i < ne * NSH; i += npt) {
+    const int el = i / NSH, dof = i % NSH, t = dof / NV, a = dof % NV;
+    if (e0 + el >= args.n_elem) continue;
+    const double* u = sU + el * NSP * NV + a;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int s = 0; s < NS; ++s) acc = fma(sXP[(s * 3 + 2) * NTPS + t], u[s * NV], acc);
+    args.fout[(e0 + el) * NSH + dof] = acc;
+  }
+}
 
 // Per-p constant tables in device memory (built by the host from the shape
 // table, pi_context.cu).
@@ -495,6 +530,8 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
           const double w8 = sW[z * NS + s], wd = w8 * __drcp_rn(det);
           const int64_t e = e0 + el;
           if (!(det > 0.0) && e < args.n_elem && flagger) flag_inverted(args.bad, args.element_id_base + e);
+          if (NE == 1 && args.fout && flagger)
+            smem[C::OFF_LDW + (el * C::NSP + s) * NZ + z] = det * w8 * load_f(args, e < args.n_elem ? e : args.n_elem - 1);
 #pragma unroll
           for (int blk = 0; blk < NE * NE; ++blk) {
             double M[16];
@@ -509,9 +546,15 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
         } else {
 #pragma unroll
           for (int k = 0; k < 16 * NE * NE; ++k) Mi[k * C::MPITCH] = 0.0;
+          if (NE == 1 && args.fout && flagger) smem[C::OFF_LDW + (el * C::NSP + s) * NZ + z] = 0.0;
         }
       }
       named_sync(kBarProd, C::NPT);
+      if (NE == 1 && C::MALL && args.fout && flagger) {
+        sumfact_load_vectors<NS, C::NSP, NZ, NV, NT, C::NTPS>(args, e0, EPC, smem + C::OFF_LDW, smem + C::OFF_LU, sXP,
+                                                            PD, ptid, C::NPT, kBarProd);
+        named_sync(kBarProd, C::NPT);
+      }
     };
     if (C::MALL && my_items > 0) {
       load_item(0);
@@ -701,6 +744,19 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) afr3[ks][mt] = sXA[(mt * KSTEPS + chunk * 3 + ks) * 32 + lane];
       const int buf = static_cast<int>(gc % C::NBUF);
+#ifndef PI_SF_NO_XPRE
+      // t'-major: the first k-step's X values (static table) before waiting for H
+      double xv0[C::TMAJOR ? MT : 1][3];
+      if constexpr (C::TMAJOR) {
+#pragma unroll
+        for (int g = 0; g < MT; ++g) {
+          const double* xp = sXP + (chunk * 4 + sl_k[0]) * 3 * NTPS + g * 8 + cpos;
+          xv0[g][0] = xp[0];
+          xv0[g][1] = xp[NTPS];
+          xv0[g][2] = xp[2 * NTPS];
+        }
+      }
+#endif
       named_sync(kBarFull0 + buf, C::NTHREADS);
       const double* Hb = sH + buf * C::H_PER_BUF;
 #pragma unroll
@@ -712,6 +768,14 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
           double xv[MT][3];
 #pragma unroll
           for (int g = 0; g < MT; ++g) {
+#ifndef PI_SF_NO_XPRE
+            if (ks == 0) {
+              xv[g][0] = xv0[g][0];
+              xv[g][1] = xv0[g][1];
+              xv[g][2] = xv0[g][2];
+              continue;
+            }
+#endif
             const double* xp = sXP + s * 3 * NTPS + g * 8 + cpos;
             xv[g][0] = xp[0];
             xv[g][1] = xp[NTPS];

@@ -39,9 +39,11 @@ struct pi_context {
   double *d_phi = nullptr, *d_pts = nullptr, *d_w = nullptr;
   double *d_xfrag = nullptr, *d_xplain = nullptr, *d_yline = nullptr, *d_tri = nullptr;
   bool tensor_ok = false;
+  int sf_ntps = 0;          // row pitch of d_xplain
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
   int p2_ctas_f[3] = {0, 0, 0};  // ... and per FP32-arithmetic instantiation
+  int p2_ctas_l[3] = {0, 0, 0};  // ... and per fused-load-vector instantiation
   // per-context rule / shape tables of the p <= 2 register kernels, passed by
   // value with every launch (kernel parameter space)
   std::unique_ptr<P2Tables> p2tab;
@@ -205,6 +207,8 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMalloc"));
   ce = cudaMemset(ctx->d_bad, 0xff, 2 * sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
+  cudaFuncSetAttribute(load_vector_sf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(sizeof(double) * kLoadSfElems * (21 + 336 + 336)));
 
   // The kernels skip the basis' structural zeros (BasisPattern): the table
   // must hold exact zeros there, as tabulate_shapes does.
@@ -224,6 +228,7 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
     SumFactHostTables tb;
     const bool ok = sumfact_build(p, n_eq, ctx->h_pts.data(), ctx->h_phi.data(), nq, nsh, tb);
     ctx->tensor_ok = ok;
+    ctx->sf_ntps = tb.ntps;
     if (ok) {
       if ((st = upload(&ctx->d_xfrag, tb.xfrag, err)) != PI_OK) return fail(st);
       if ((st = upload(&ctx->d_xplain, tb.xplain, err)) != PI_OK) return fail(st);
@@ -315,6 +320,18 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
     ctx->p2_ctas_f[0] = ctas(p2_lane_kernel<false, true, float>, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES);
     ctx->p2_ctas_f[1] = ctas(p2_lane_kernel<true, true, float>, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES);
     ctx->p2_ctas_f[2] = ctas(p2_lane_kernel<true, false, float>, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES);
+    cudaFuncSetAttribute(p2_lane_kernel<false, true, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<false, true>::SMEM_BYTES_LOAD));
+    cudaFuncSetAttribute(p2_lane_kernel<true, true, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, true>::SMEM_BYTES_LOAD));
+    cudaFuncSetAttribute(p2_lane_kernel<true, false, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P2Cfg<true, false>::SMEM_BYTES_LOAD));
+    ctx->p2_ctas_l[0] = ctas(p2_lane_kernel<false, true, double, true>, P2Cfg<false, true>::NTHREADS,
+                             P2Cfg<false, true>::SMEM_BYTES_LOAD);
+    ctx->p2_ctas_l[1] = ctas(p2_lane_kernel<true, true, double, true>, P2Cfg<true, true>::NTHREADS,
+                             P2Cfg<true, true>::SMEM_BYTES_LOAD);
+    ctx->p2_ctas_l[2] = ctas(p2_lane_kernel<true, false, double, true>, P2Cfg<true, false>::NTHREADS,
+                             P2Cfg<true, false>::SMEM_BYTES_LOAD);
     ctx->p2_ok = true;
   }
   ce = cudaGetLastError();
@@ -370,7 +387,8 @@ namespace {
 // pi_integrate / pi_integrate_f32: exactly one of out, out32 is non-NULL.
 pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
                          int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
-                         float* out32, int out_layout, int64_t ld_out, void* stream, pi_error_info* err) {
+                         float* out32, int out_layout, int64_t ld_out, void* stream, pi_error_info* err,
+                         const double* f = nullptr, double f_const = 0.0, double* fout = nullptr) {
   if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
   if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
   if (n_elem < 0) return set_error(err, PI_E_CONTRACT, "n_elem < 0");
@@ -392,7 +410,12 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   a.ld_out = ld_out;
   a.bad = ctx->d_bad;
   a.bad_mat = ctx->d_bad + 1;
+  a.fout = fout;
+  a.fsrc = f;
+  a.fconst = f_const;
   const int ne = ctx->n_eq, ncoef = 16 * ne * ne;
+  if (fout && (ne != 1 || out32))
+    return set_error(err, PI_E_CONFIG, "fused load vectors need a scalar weak form (n_eq = 1) and FP64 output");
   bool general = false, symmetric = true;
   int form = kFormLaplace;
   switch (coeff_mode) {
@@ -468,6 +491,17 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
         p2_lane_kernel<true, true, float><<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES, s>>>(a, tb);
       else
         p2_lane_kernel<true, false, float><<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES, s>>>(a, tb);
+    } else if (fout) {
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas_l[which]));
+      if (!general)
+        p2_lane_kernel<false, true, double, true>
+            <<<grid, P2Cfg<false, true>::NTHREADS, P2Cfg<false, true>::SMEM_BYTES_LOAD, s>>>(a, tb);
+      else if (symmetric)
+        p2_lane_kernel<true, true, double, true>
+            <<<grid, P2Cfg<true, true>::NTHREADS, P2Cfg<true, true>::SMEM_BYTES_LOAD, s>>>(a, tb);
+      else
+        p2_lane_kernel<true, false, double, true>
+            <<<grid, P2Cfg<true, false>::NTHREADS, P2Cfg<true, false>::SMEM_BYTES_LOAD, s>>>(a, tb);
     } else {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(groups, ctx->p2_ctas[which]));
       if (!general)
@@ -479,13 +513,16 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
     }
   } else if (v == PI_VARIANT_DENSE && ne == 1) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
-    if (general) {
-      constexpr int T = p1_threads<true>();
-      p1_thread_kernel<true><<<static_cast<unsigned>((n_elem + T - 1) / T), T, 0, s>>>(a, t);
-    } else {
-      constexpr int T = p1_threads<false>();
-      p1_thread_kernel<false><<<static_cast<unsigned>((n_elem + T - 1) / T), T, 0, s>>>(a, t);
-    }
+    constexpr int TG = p1_threads<true>(), TL = p1_threads<false>();
+    const unsigned gg = static_cast<unsigned>((n_elem + TG - 1) / TG), gl = static_cast<unsigned>((n_elem + TL - 1) / TL);
+    if (general && fout)
+      p1_thread_kernel<true, true><<<gg, TG, 0, s>>>(a, t);
+    else if (general)
+      p1_thread_kernel<true><<<gg, TG, 0, s>>>(a, t);
+    else if (fout)
+      p1_thread_kernel<false, true><<<gl, TL, 0, s>>>(a, t);
+    else
+      p1_thread_kernel<false><<<gl, TL, 0, s>>>(a, t);
   } else {
     SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
     sumfact_launch(ctx->p, ne, form, symmetric, a, t, s);
@@ -521,6 +558,18 @@ pi_status pi_integrate_f32(pi_context* ctx, int64_t n_elem, int64_t element_id_b
                         out_layout, ld_out, stream, err);
 }
 
+pi_status pi_integrate_load(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
+                            int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
+                            int out_layout, int64_t ld_out, const double* f, double f_const, double* load_out,
+                            void* stream, pi_error_info* err) {
+  if ((!out || !load_out) && n_elem > 0) {
+    if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+    return set_error(err, PI_E_CONTRACT, "stiffness and load-vector output buffers must be non-NULL");
+  }
+  return integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, out, nullptr,
+                        out_layout, ld_out, stream, err, f, f_const, load_out);
+}
+
 pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
                           int64_t geom_ld, const double* f, double f_const, double* out, void* stream,
                           pi_error_info* err) {
@@ -539,9 +588,18 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
   DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   PI_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
-  const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);
-  load_vector_kernel<<<grid, 32 * kLoadWarps, sizeof(double) * kLoadWarps * ctx->n_q, s>>>(a, t, ctx->n_q,
-                                                                                            ctx->n_shape, f, f_const);
+  if (ctx->tensor_ok) {  // sum-factorised: X_2 and P tables instead of the dense phi table
+    const int ns = ctx->n_q / (ctx->p + 1);
+    LoadSfTables lt{ctx->d_tri, ctx->d_yline, ctx->d_xplain, ctx->d_w, ns, ctx->p + 1, ctx->p + 1,
+                    ctx->n_shape / (ctx->p + 1), ctx->sf_ntps};
+    const size_t smem = sizeof(double) * kLoadSfElems * (21 + ctx->n_q + ns * (ctx->p + 1));
+    const unsigned grid = static_cast<unsigned>((n_elem + kLoadSfElems - 1) / kLoadSfElems);
+    load_vector_sf_kernel<<<grid, kLoadSfThreads, smem, s>>>(a, lt, f, f_const);
+  } else {
+    const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);
+    load_vector_kernel<<<grid, 32 * kLoadWarps, sizeof(double) * kLoadWarps * ctx->n_q, s>>>(a, t, ctx->n_q,
+                                                                                              ctx->n_shape, f, f_const);
+  }
   PI_CUDA(cudaGetLastError(), "load-vector launch");
   ctx->calls.push_back({geom, geom_ld, element_id_base, n_elem});
   return mark_stream(ctx, s, err);

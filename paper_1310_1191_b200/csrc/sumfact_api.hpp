@@ -15,6 +15,7 @@ struct SumFactTables;
 
 struct SumFactHostTables {
   std::vector<double> xfrag, xplain, yline, tri;
+  int ntps = 0;  // row pitch of xplain ([NSP][3][ntps])
 };
 
 // True if (p, n_eq) has a sum-factorised instantiation.

@@ -47,14 +47,21 @@ struct SumFactHost {
   template <int FORM, bool SYM>
   static void attr() {
     cudaFuncSetAttribute(sumfact_kernel<P, NE, FORM, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(CK<SYM>::SMEM_BYTES));
+                         static_cast<int>(smem_bytes<SYM>(NE == 1)));
   }
+  // dynamic shared memory of a launch (fused load vectors: the dw / u region after the rest)
+  template <bool SYM>
+  static constexpr size_t smem_bytes(bool load) {
+    return load ? CK<SYM>::SMEM_BYTES_LOAD : CK<SYM>::SMEM_BYTES;
+  }
+  static_assert(NE != 1 || (CK<false>::SMEM_BYTES_LOAD <= 232448 && CK<true>::SMEM_BYTES_LOAD <= 232448),
+                "fused load-vector region must fit the SM");
   // Persistent grid: as many CTAs as fit on the device at once (queried per
   // instantiation), each looping over (element group, a'-group, column block) items.
   template <int FORM, bool SYM>
-  static int resident_ctas() {
-    static std::atomic<int> cache[kMaxDevices] = {};
-    return persistent_grid(cache, sumfact_kernel<P, NE, FORM, SYM>, CK<SYM>::NTHREADS, CK<SYM>::SMEM_BYTES);
+  static int resident_ctas(bool load) {
+    static std::atomic<int> cache[2][kMaxDevices] = {};
+    return persistent_grid(cache[load], sumfact_kernel<P, NE, FORM, SYM>, CK<SYM>::NTHREADS, smem_bytes<SYM>(load));
   }
   // symmetric forms at high p: the pair-split kernel (kernels_pairs.cuh)
   // (measured: faster for scalar forms at p >= 5; slower for n_eq = 3, whose
@@ -65,18 +72,22 @@ struct SumFactHost {
   static constexpr bool kPairs = NE == 1 && P >= PI_PAIRS_MINP;
   template <int FORM>
   static void attr_pairs() {
-    if constexpr (kPairs)
+    if constexpr (kPairs) {
+      static_assert(PairsConfig<P, NE>::SMEM_BYTES_LOAD <= 232448, "fused load-vector region must fit the SM");
       cudaFuncSetAttribute(sumfact_pairs_kernel<P, NE, FORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(PairsConfig<P, NE>::SMEM_BYTES));
+                           static_cast<int>(PairsConfig<P, NE>::SMEM_BYTES_LOAD));
+    }
   }
   template <int FORM>
   static bool go_pairs(const LaunchArgs& a, const SumFactTables& t, cudaStream_t s) {
     if constexpr (kPairs) {
       using PC = PairsConfig<P, NE>;
-      static std::atomic<int> cache[kMaxDevices] = {};
-      const int c = persistent_grid(cache, sumfact_pairs_kernel<P, NE, FORM>, PC::NTHREADS, PC::SMEM_BYTES);
+      static std::atomic<int> cache[2][kMaxDevices] = {};
+      const bool load = a.fout != nullptr;
+      const size_t smem = load ? PC::SMEM_BYTES_LOAD : PC::SMEM_BYTES;
+      const int c = persistent_grid(cache[load], sumfact_pairs_kernel<P, NE, FORM>, PC::NTHREADS, smem);
       const dim3 grid(static_cast<unsigned>(std::min<int64_t>(a.n_elem, c)));  // element-major CTAs
-      sumfact_pairs_kernel<P, NE, FORM><<<grid, PC::NTHREADS, PC::SMEM_BYTES, s>>>(a, t);
+      sumfact_pairs_kernel<P, NE, FORM><<<grid, PC::NTHREADS, smem, s>>>(a, t);
       return true;
     }
     return false;
@@ -88,9 +99,10 @@ struct SumFactHost {
       if (go_pairs<FORM>(a, t, s)) return;
 #endif
     using K = CK<SYM>;
+    const bool load = NE == 1 && a.fout != nullptr;
     const int64_t items = (a.n_elem + K::EPC - 1) / K::EPC * K::NITEM;
-    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<FORM, SYM>())));
-    sumfact_kernel<P, NE, FORM, SYM><<<grid, K::NTHREADS, K::SMEM_BYTES, s>>>(a, t);
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(items, resident_ctas<FORM, SYM>(load))));
+    sumfact_kernel<P, NE, FORM, SYM><<<grid, K::NTHREADS, smem_bytes<SYM>(load), s>>>(a, t);
   }
 
   // Builds the X fragment table, Y table and rule coordinates from the
@@ -156,6 +168,7 @@ struct SumFactHost {
           out.xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
         }
     out.xplain.assign(C::XPLAIN, 0.0);
+    out.ntps = C::NTPS;
     for (int s = 0; s < NS; ++s)
       for (int t = 0; t < NT; ++t)
         for (int x = 0; x < 3; ++x)
