@@ -666,18 +666,25 @@ def main_ours(args, ws, rank, local):
             nsh = pb.shape_count(p)
             fbuf = torch.empty(E * nsh, dtype=torch.float64, device=dev)
             R.ensure_out(R.chunk(p, form) * R.kk(p, form))
-            ms_fused = timed(lambda: R.one_pass(p, form, load=(fbuf, fvals)))
             it = R.ctx(p, form)
+            it.set_load_fusion(pb.LOAD_FUSED)
+            ms_fused = timed(lambda: R.one_pass(p, form, load=(fbuf, fvals)))
+            it.set_load_fusion(pb.LOAD_SEPARATE)
+            ms_sep = timed(lambda: R.one_pass(p, form, load=(fbuf, fvals)))
+            it.set_load_fusion(pb.LOAD_AUTO)
             ms_alone = timed(lambda: it.load_vectors_device(E, R.geom, fbuf, f=fvals, stream=R.sptr))
             it.check()
-            entry = {"fused_elements_per_s": ws * E / (ms_fused * 1e-3), "fused_ms": ms_fused,
-                     "stiffness_only_ms": per_p_ms[p], "fusion_overhead": ms_fused / per_p_ms[p] - 1.0,
-                     "standalone_elements_per_s": ws * E / (ms_alone * 1e-3), "standalone_ms": ms_alone,
-                     "standalone_hbm_gbs": (144 + 8 + 8 * nsh) * E / (ms_alone * 1e-3) / 1e9}
+            entry = {"stiffness_only_ms": per_p_ms[p],
+                     "fused_ms": ms_fused, "fused_elements_per_s": ws * E / (ms_fused * 1e-3),
+                     "fusion_overhead": ms_fused / per_p_ms[p] - 1.0,
+                     "separate_ms": ms_sep, "separate_elements_per_s": ws * E / (ms_sep * 1e-3),
+                     "auto": "fused" if p == 1 else "separate",
+                     "load_kernel_ms": ms_alone, "load_kernel_elements_per_s": ws * E / (ms_alone * 1e-3),
+                     "load_kernel_hbm_gbs": (144 + 8 + 8 * nsh) * E / (ms_alone * 1e-3) / 1e9}
             if not args.no_parity:
                 # F = f * column 0 of the c[0][0][0][0] = 1 mass matrix (the reference's integrate_generic)
                 lidx = sample_indices(E, 64)
-                R.one_pass(p, form, load=(fbuf, fvals))
+                R.one_pass(p, form, load=(fbuf, fvals))  # the AUTO strategy
                 torch.cuda.synchronize(dev)
                 got = fbuf.view(E, nsh)[lidx].cpu().numpy()
                 sys.path.insert(0, str(ROOT / "tests"))

@@ -74,7 +74,10 @@ enum {
 enum {
   PI_VARIANT_AUTO = 0,     /* best measured strategy for (p, n_eq, coefficients) */
   PI_VARIANT_DENSE = 1,    /* per-point B^T (dw C) B accumulation (the reference's loop nest) */
-  PI_VARIANT_SUMFACT = 2   /* tensor-product (sum-factorised) contraction on FP64 DMMA */
+  PI_VARIANT_SUMFACT = 2,  /* tensor-product (sum-factorised) contraction on FP64 DMMA */
+  PI_VARIANT_TC32 = 3      /* scalar forms, p = 3..7: FP32-output calls run the sum-factorised
+                              contraction on the tcgen05 tensor cores (3xTF32, TMEM accumulators;
+                              bound 5e-5, measured ~4e-7); FP64 calls as PI_VARIANT_SUMFACT */
 };
 
 /* ---- per-p constants: the product's own restatement of the reference ---- */
@@ -144,16 +147,23 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
                           const double* geom, int64_t geom_ld, const double* f, double f_const,
                           double* out, void* stream, pi_error_info* err);
 
-/* pi_integrate with the load vectors fused into the same pass (scalar weak
- * forms, n_eq = 1, FP64): besides K, writes F_i = sum_q det*w_q * f * phi_i(x_q)
- * to load_out (device [n_elem][n_shape]) from the Jacobians the stiffness
- * kernel already forms -- no second read of the geometry.  f / f_const as in
+/* pi_integrate plus the load vectors in the same call (scalar weak forms,
+ * n_eq = 1, FP64): besides K, writes F_i = sum_q det*w_q * f * phi_i(x_q) to
+ * load_out (device [n_elem][n_shape]); fused into the stiffness kernel (F
+ * from the Jacobians it already forms, no second read of the geometry) or as
+ * a second launch, per pi_context_set_load_fusion.  f / f_const as in
  * pi_load_vectors.  Same bound as pi_load_vectors: F equals f times column 0
  * of the c[0][0][0][0] = 1 mass matrix of integrate_generic. */
 pi_status pi_integrate_load(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
                             int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
                             int out_layout, int64_t ld_out, const double* f, double f_const, double* load_out,
                             void* stream, pi_error_info* err);
+
+/* pi_integrate_load strategy: AUTO = fused at p = 1, a second (sum-factorised,
+ * geometry re-reading) launch at p >= 2, where the measured fusion overhead on
+ * the stiffness kernel exceeds the cost of the extra launch. */
+enum { PI_LOAD_AUTO = 0, PI_LOAD_FUSED = 1, PI_LOAD_SEPARATE = 2 };
+pi_status pi_context_set_load_fusion(pi_context* ctx, int mode, pi_error_info* err);
 
 /* Waits for the context's outstanding work and reports inverted elements
  * (PI_E_INVERTED_ELEMENT with element/det/xi filled) or CUDA errors. */

@@ -28,7 +28,7 @@ __all__ = [
     "Error", "ConfigError", "DomainError", "UnsupportedDegreeError", "InvertedElementError",
     "CapacityError", "SharedMemoryError", "ContractViolation", "IoError", "CudaError",
     "LAPLACE", "UNIFORM", "PER_ELEMENT", "ELASTICITY", "ELASTICITY_UNIFORM", "OUT_CANONICAL", "OUT_SOA",
-    "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT",
+    "VARIANT_AUTO", "VARIANT_DENSE", "VARIANT_SUMFACT", "VARIANT_TC32", "LOAD_AUTO", "LOAD_FUSED", "LOAD_SEPARATE",
     "shape_count", "quadrature_point_count", "prism_quadrature", "tabulate_shapes",
     "generate_box_mesh", "generate_cdr_coefficients", "generate_materials", "laplace_tensor",
     "Integrator", "run_batch", "integrate_host_multi", "measure_fp64_peak", "PRISTIF1", "PRISTIF2", "save_stiffness", "load_stiffness",
@@ -43,7 +43,8 @@ LAPLACE, UNIFORM, PER_ELEMENT = 0, 1, 2
 # (device SoA [2][ld] / host AoS [n][2]) or one material for all elements (host [2]).
 ELASTICITY, ELASTICITY_UNIFORM = 3, 4
 OUT_CANONICAL, OUT_SOA = 0, 1
-VARIANT_AUTO, VARIANT_DENSE, VARIANT_SUMFACT = 0, 1, 2
+VARIANT_AUTO, VARIANT_DENSE, VARIANT_SUMFACT, VARIANT_TC32 = 0, 1, 2, 3
+LOAD_AUTO, LOAD_FUSED, LOAD_SEPARATE = 0, 1, 2
 
 
 # ---- errors: prismint::errc (errors.hpp:10-19) plus CUDA ----
@@ -133,6 +134,7 @@ def library():
                                     C.POINTER(vp), E]
     L.pi_context_destroy.argtypes = [vp]
     L.pi_context_set_variant.argtypes = [vp, C.c_int, E]
+    L.pi_context_set_load_fusion.argtypes = [vp, C.c_int, E]
     L.pi_context_variant.argtypes = [vp, C.c_int]
     L.pi_context_stream.argtypes = [vp]
     L.pi_context_stream.restype = vp
@@ -374,6 +376,11 @@ class Integrator:
     def set_variant(self, variant):
         err = _ErrInfo()
         _raise(library().pi_context_set_variant(self._h, variant, C.byref(err)), err)
+
+    def set_load_fusion(self, mode):
+        """LOAD_AUTO / LOAD_FUSED / LOAD_SEPARATE: strategy of integrate_device(load_out=...)."""
+        err = _ErrInfo()
+        _raise(library().pi_context_set_load_fusion(self._h, mode, C.byref(err)), err)
 
     def variant(self, coeff_mode=LAPLACE):
         return library().pi_context_variant(self._h, coeff_mode)

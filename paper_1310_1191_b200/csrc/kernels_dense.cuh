@@ -57,19 +57,24 @@ struct BasisPattern {
 // skipped at compile time (13 of the 24 phi entries per point are non-zero),
 // so the contraction costs about half the dense loop nest's FMAs.
 // LOAD: also the load vector F_i = sum_q det w_q f phi_0(i, q) (6 more accumulators).
-template <bool GENERAL, bool LOAD = false>
+// T = float: the FP32 arithmetic variant (pi_integrate_f32): Jacobian and
+// point block in FP64, rounded once per point; phi, the accumulation, the
+// staging and the stores in FP32 (half the registers, staging and bytes).
+template <bool GENERAL, bool LOAD = false, typename T = double>
 __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : PI_P1_MINB)
     p1_thread_kernel(LaunchArgs args, DenseTables tab) {
   constexpr int kP1Threads = p1_threads<GENERAL>();
   constexpr int NQ = 6, NSH = 6, KK = NSH * NSH;
+  constexpr bool F32 = sizeof(T) == 4;
+  static_assert(!(F32 && LOAD), "fused load vectors are FP64");
   using BP = BasisPattern<1>;
-  __shared__ double sPhi[NQ * 4 * NSH];
+  __shared__ T sPhi[NQ * 4 * NSH];
   __shared__ double sPts[NQ * 3];
   __shared__ double sW[NQ];
   __shared__ __align__(16) double sOut[kP1Threads * KK + kP1Threads];  // 36 KB staging
 
   const int tid = threadIdx.x;
-  for (int i = tid; i < NQ * 4 * NSH; i += kP1Threads) sPhi[i] = tab.phi[i];
+  for (int i = tid; i < NQ * 4 * NSH; i += kP1Threads) sPhi[i] = static_cast<T>(tab.phi[i]);
   if (tid < NQ * 3) sPts[tid] = tab.pts[tid];
   if (tid < NQ) sW[tid] = tab.w[tid];
   __syncthreads();
@@ -98,9 +103,9 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
     for (int c = 0; c < 16; ++c) cf[c] = args.coeff ? args.coeff[c * args.coeff_ld + ec] : args.cu[c];
   }
 
-  double K[KK];
+  T K[KK];
 #pragma unroll
-  for (int i = 0; i < KK; ++i) K[i] = 0.0;
+  for (int i = 0; i < KK; ++i) K[i] = T(0);
   double F[LOAD ? NSH : 1];
   const double fe = LOAD ? load_f(args, ec) : 0.0;
 #pragma unroll
@@ -109,10 +114,13 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
 
 #pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
-    double M[16];
-    const double det = point_block<GENERAL>(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], sW[q], cf, M);
+    double Md[16];
+    const double det = point_block<GENERAL>(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], sW[q], cf, Md);
     inverted |= !(det > 0.0);
-    const double* ph = sPhi + q * 4 * NSH;
+    T M[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) M[k] = static_cast<T>(Md[k]);
+    const T* ph = sPhi + q * 4 * NSH;
     if constexpr (LOAD) {
       const double dwf = det * sW[q] * fe;
 #pragma unroll
@@ -122,10 +130,10 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
     // G_l(i) = sum_k phi_k(i) M_kl ; K_ij += sum_l G_l(i) phi_l(j)
 #pragma unroll
     for (int i = 0; i < NSH; ++i) {
-      double g[4];
+      T g[4];
 #pragma unroll
       for (int l = K0; l < 4; ++l) {
-        double s = 0.0;
+        T s = T(0);
 #pragma unroll
         for (int k = K0; k < 4; ++k)
           if (BP::nz(k, i)) s = fma(ph[k * NSH + i], M[k * 4 + l], s);
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
       }
 #pragma unroll
       for (int j = GENERAL ? 0 : i; j < NSH; ++j) {
-        double s = K[i * NSH + j];
+        T s = K[i * NSH + j];
 #pragma unroll
         for (int l = K0; l < 4; ++l)
           if (BP::nz(l, j)) s = fma(g[l], ph[l * NSH + j], s);
@@ -160,6 +168,40 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
     }
     return;
   }
+  if constexpr (F32) {
+    // FP32 staging [thread][36] (odd float2 pitch 19: conflict-free), then the
+    // CTA's contiguous block (144 B per element): one TMA bulk store when the
+    // output base is 16-byte aligned, else coalesced 8- / 4-byte stores.
+    constexpr int P2F = KK / 2 + 1;
+    static_assert(kP1Threads * (P2F + KK / 2) <= kP1Threads * KK + kP1Threads, "FP32 staging fits sOut");
+    float2* so = reinterpret_cast<float2*>(sOut);
+    __syncthreads();  // every thread is done with its edge vectors / coefficients
+#pragma unroll
+    for (int i = 0; i < KK / 2; ++i) so[tid * P2F + i] = make_float2(K[2 * i], K[2 * i + 1]);
+    __syncthreads();
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * kP1Threads;
+    const int n_here = static_cast<int>(min(static_cast<int64_t>(kP1Threads), args.n_elem - first));
+    float2* pk = reinterpret_cast<float2*>(sOut) + kP1Threads * P2F;  // packed image after the padded staging
+    for (int i = tid; i < n_here * (KK / 2); i += kP1Threads) pk[i] = so[(i / (KK / 2)) * P2F + i % (KK / 2)];
+    __syncthreads();
+    const uintptr_t ob = reinterpret_cast<uintptr_t>(args.out32 + first * KK);
+    if ((ob & 15) == 0) {
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        bulk_store(reinterpret_cast<double*>(args.out32 + first * KK), reinterpret_cast<const double*>(pk),
+                   static_cast<unsigned>(n_here) * KK * 4u);
+        bulk_commit();
+        bulk_wait_read();
+      }
+    } else if ((ob & 7) == 0) {
+      float2* dst = reinterpret_cast<float2*>(args.out32 + first * KK);
+      for (int i = tid; i < n_here * (KK / 2); i += kP1Threads) dst[i] = pk[i];
+    } else {
+      const float* src = reinterpret_cast<const float*>(pk);
+      for (int i = tid; i < n_here * KK; i += kP1Threads) args.out32[first * KK + i] = src[i];
+    }
+    return;
+  } else {
   // Canonical: stage [thread][36] in smem (odd stride in 16B units avoids
   // bank conflicts: 36 doubles = 18 x 16 B), then write the CTA's contiguous
   // block of 128 * 288 B with coalesced 16-byte stores.
@@ -201,6 +243,7 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
       for (int i = tid; i < 2 * total2; i += kP1Threads) args.out[first * KK + i] = sOut[i];
     }
   }
+  }
 }
 
 // Load vectors: F_i = sum_q det_q w_q f phi_i(q) (value row).  One warp per
@@ -238,10 +281,13 @@ __global__ void __launch_bounds__(32 * kLoadWarps)
 // sum-factorisation tables): phi_0(t*NV + a, (s, z)) = m_t(s) P_a(z), so
 //     F(t,a) = sum_s X_2(t,s) u(s,a),   u(s,a) = sum_z P_a(z) dw(s,z),
 // dw = det w f at every rule point (q = z*NS + s, reference order).  A CTA
-// takes kLoadSfElems elements: edge vectors, dw and u per element in shared
-// memory; F leaves as one contiguous coalesced block per CTA.  Per element
-// the kernel reads 144 B of geometry (+8 B of f) and writes 8 N_sh bytes: an
-// HBM-bound stream (the per-p tables are a few KB and stay in L1).
+// takes kLoadSfElems elements: (1) coalesced SoA geometry into shared memory,
+// (2) one thread per (element, triangle point s) walks the NZ Gauss points:
+// det, dw and u(s, .) in registers, (3) one thread per (element, dof) forms F
+// and stores it (consecutive dofs of consecutive elements: coalesced).  Per
+// element: 144 B of geometry (+8 B of f) read, 8 N_sh bytes written, N_q
+// determinants -- HBM-bound at low p, FP64-bound at high p; the per-p tables
+// are a few KB and stay in L1.
 struct LoadSfTables {
   const double* tri;     // xi1 [NS], xi2 [NS]
   const double* yline;   // (P, P') [NZ][NV] pairs, xi3 [NZ]
@@ -249,46 +295,54 @@ struct LoadSfTables {
   const double* w;       // [NQ] reference order
   int ns, nz, nv, nt, ntps;
 };
-constexpr int kLoadSfElems = 16, kLoadSfThreads = 256;
+constexpr int kLoadSfThreads = 256;
+// elements per CTA: 64 at p <= 4, fewer where u (NS x NV per element) grows
+constexpr int load_sf_elems(int ns, int nv) { return ns * nv <= 80 ? 64 : ns * nv <= 150 ? 32 : 16; }
+constexpr size_t load_sf_smem(int ns, int nv) {
+  return sizeof(double) * (18 * (load_sf_elems(ns, nv) + 1) + load_sf_elems(ns, nv) * ns * nv);
+}
 __global__ void __launch_bounds__(kLoadSfThreads)
     load_vector_sf_kernel(LaunchArgs args, LoadSfTables tb, const double* f, double f_const) {
-  const int ns = tb.ns, nz = tb.nz, nv = tb.nv, nt = tb.nt, nq = ns * nz, nsh = nt * nv;
+  const int ns = tb.ns, nz = tb.nz, nv = tb.nv, nt = tb.nt, nsh = nt * nv;
+  const int kLoadSfElems = load_sf_elems(ns, nv), kLoadSfPitch = kLoadSfElems + 1;
   extern __shared__ __align__(16) double sl[];
-  double* sD = sl;                          // [E][21]
-  double* sDW = sD + kLoadSfElems * 21;     // [E][nq]
-  double* sU = sDW + kLoadSfElems * nq;     // [E][ns][nv]
+  double* sX = sl;                          // vertices [18][kLoadSfPitch]
+  double* sU = sX + 18 * kLoadSfPitch;      // u [E][ns][nv]
   const int tid = threadIdx.x;
   const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kLoadSfElems;
   const int64_t left = args.n_elem - e0;
   const int ne = left < kLoadSfElems ? static_cast<int>(left) : kLoadSfElems;
-  if (tid < ne) {
+  for (int i = tid; i < 18 * kLoadSfElems; i += kLoadSfThreads) {
+    const int c = i / kLoadSfElems, el = i % kLoadSfElems;
+    if (el < ne) sX[c * kLoadSfPitch + el] = args.geom[c * args.geom_ld + e0 + el];
+  }
+  __syncthreads();
+  for (int i = tid; i < ne * ns; i += kLoadSfThreads) {
+    const int el = i / ns, s = i - el * ns;
     double x[18], d[21];
 #pragma unroll
-    for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e0 + tid];
+    for (int c = 0; c < 18; ++c) x[c] = sX[c * kLoadSfPitch + el];
     prism_edges(x, d);
-#pragma unroll
-    for (int c = 0; c < 21; ++c) sD[tid * 21 + c] = d[c];
-  }
-  __syncthreads();
-  for (int i = tid; i < ne * nq; i += kLoadSfThreads) {
-    const int el = i / nq, q = i - el * nq, z = q / ns, s = q - z * ns;
-    double cf[3][3];
-    const double det = jacobian_cofactors(sD + el * 21, __ldg(tb.tri + s), __ldg(tb.tri + ns + s),
-                                          __ldg(tb.yline + 2 * nv * nz + z), cf);
-    if (!(det > 0.0)) flag_inverted(args.bad, args.element_id_base + e0 + el);
     const double fe = f ? f[e0 + el] : f_const;
-    sDW[el * nq + s * nz + z] = det * __ldg(tb.w + q) * fe;
+    const double xi1 = __ldg(tb.tri + s), xi2 = __ldg(tb.tri + ns + s);
+    double u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool inverted = false;
+    for (int z = 0; z < nz; ++z) {
+      double cf[3][3];
+      const double det = jacobian_cofactors(d, xi1, xi2, __ldg(tb.yline + 2 * nv * nz + z), cf);
+      inverted |= !(det > 0.0);
+      const double dw = det * __ldg(tb.w + z * ns + s) * fe;
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (a < nv) u[a] = fma(__ldg(tb.yline + 2 * (z * nv + a)), dw, u[a]);
+    }
+    if (inverted) flag_inverted(args.bad, args.element_id_base + e0 + el);
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+      if (a < nv) sU[(el * ns + s) * nv + a] = u[a];
   }
   __syncthreads();
-  for (int i = tid; i < ne * ns * nv; i += kLoadSfThreads) {
-    const int el = i / (ns * nv), r = i - el * ns * nv, s = r / nv, a = r - s * nv;
-    const double* dw = sDW + el * nq + s * nz;
-    double u = 0.0;
-    for (int z = 0; z < nz; ++z) u = fma(__ldg(tb.yline + 2 * (z * nv + a)), dw[z], u);
-    sU[(el * ns + s) * nv + a] = u;
-  }
-  __syncthreads();
-  for (int i = tid; i < ne * nsh; i += kLoadSfThreads) {  // coalesced: consecutive dofs of consecutive elements
+  for (int i = tid; i < ne * nsh; i += kLoadSfThreads) {
     const int el = i / nsh, dof = i - el * nsh, t = dof / nv, a = dof - t * nv;
     const double* u = sU + el * ns * nv + a;
     double acc = 0.0;

@@ -15,6 +15,8 @@
 #include "kernels_p2.cuh"
 #include "kernels_sumfact.cuh"
 #include "sumfact_api.hpp"
+#include "tc32_api.hpp"
+#include "kernels_tc32.cuh"
 #include "pi_internal.hpp"
 
 using namespace pib;
@@ -34,11 +36,16 @@ struct StreamMark {
 struct pi_context {
   int device = 0, p = 0, n_eq = 1, n_q = 0, n_shape = 0;
   int variant = PI_VARIANT_AUTO;
+  int load_fusion = PI_LOAD_AUTO;  // pi_integrate_load strategy
   cudaStream_t stream = nullptr;
   std::vector<double> h_pts, h_w, h_phi;
   double *d_phi = nullptr, *d_pts = nullptr, *d_w = nullptr;
   double *d_xfrag = nullptr, *d_xplain = nullptr, *d_yline = nullptr, *d_tri = nullptr;
   bool tensor_ok = false;
+  // FP32 variant on tcgen05 (kernels_tc32.cuh), p = 3..7 scalar forms
+  bool tc_ok = false;
+  float *d_tc_bhi = nullptr, *d_tc_blo = nullptr, *d_tc_xg = nullptr, *d_tc_y = nullptr;
+  double* d_tc_z = nullptr;
   int sf_ntps = 0;          // row pitch of d_xplain
   bool p2_ok = false;       // p = 2 register-dense kernel available
   int p2_ctas[3] = {0, 0, 0};  // persistent grid per p2_lane_kernel instantiation
@@ -135,6 +142,7 @@ pi_status mark_stream(pi_context* ctx, cudaStream_t s, pi_error_info* err) {
 }
 
 int resolve_variant(const pi_context* ctx) {
+  if (ctx->variant == PI_VARIANT_TC32) return PI_VARIANT_SUMFACT;  // FP64 calls: the DMMA kernels
   if (ctx->variant != PI_VARIANT_AUTO) return ctx->variant;
   if ((ctx->n_eq == 1 && ctx->p <= 2) || (ctx->n_eq == 3 && ctx->p <= 3)) return PI_VARIANT_DENSE;
   return ctx->tensor_ok ? PI_VARIANT_SUMFACT : PI_VARIANT_DENSE;
@@ -208,7 +216,7 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   ce = cudaMemset(ctx->d_bad, 0xff, 2 * sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
   cudaFuncSetAttribute(load_vector_sf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(sizeof(double) * kLoadSfElems * (21 + 336 + 336)));
+                       64 * 1024);  // >= load_sf_smem at every p
 
   // The kernels skip the basis' structural zeros (BasisPattern): the table
   // must hold exact zeros there, as tabulate_shapes does.
@@ -235,6 +243,18 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
       if ((st = upload(&ctx->d_yline, tb.yline, err)) != PI_OK) return fail(st);
       if ((st = upload(&ctx->d_tri, tb.tri, err)) != PI_OK) return fail(st);
       sumfact_set_attrs(p, n_eq);
+      if (tc32_supported(p, n_eq)) {
+        Tc32HostTables tt;
+        if (tc32_build(p, ctx->h_pts.data(), ctx->h_phi.data(), nq, nsh, tt)) {
+          if ((st = upload(&ctx->d_tc_bhi, tt.bhi, err)) != PI_OK) return fail(st);
+          if ((st = upload(&ctx->d_tc_blo, tt.blo, err)) != PI_OK) return fail(st);
+          if ((st = upload(&ctx->d_tc_xg, tt.xg, err)) != PI_OK) return fail(st);
+          if ((st = upload(&ctx->d_tc_y, tt.yline, err)) != PI_OK) return fail(st);
+          if ((st = upload(&ctx->d_tc_z, tt.z, err)) != PI_OK) return fail(st);
+          tc32_attrs(p);
+          ctx->tc_ok = true;
+        }
+      }
     } else {
       return fail(set_error(err, PI_E_CONFIG,
                             "shape table / rule are not the tensor-product prism basis the kernels factorise"));
@@ -353,6 +373,11 @@ pi_status pi_context_destroy(pi_context* ctx) {
   cudaFree(ctx->d_xplain);
   cudaFree(ctx->d_yline);
   cudaFree(ctx->d_tri);
+  cudaFree(ctx->d_tc_bhi);
+  cudaFree(ctx->d_tc_blo);
+  cudaFree(ctx->d_tc_xg);
+  cudaFree(ctx->d_tc_y);
+  cudaFree(ctx->d_tc_z);
   cudaFree(ctx->d_bad);
   cudaFree(ctx->d_pts4);
   for (auto& m : ctx->marks) cudaEventDestroy(m.done);
@@ -364,8 +389,10 @@ pi_status pi_context_destroy(pi_context* ctx) {
 
 pi_status pi_context_set_variant(pi_context* ctx, int variant, pi_error_info* err) {
   if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
-  if (variant < PI_VARIANT_AUTO || variant > PI_VARIANT_SUMFACT)
+  if (variant < PI_VARIANT_AUTO || variant > PI_VARIANT_TC32)
     return set_error(err, PI_E_CONFIG, "unknown variant %d", variant);
+  if (variant == PI_VARIANT_TC32 && !ctx->tc_ok)
+    return set_error(err, PI_E_CONFIG, "the tcgen05 FP32 kernels need a scalar weak form at p = 3..7");
   if (variant == PI_VARIANT_SUMFACT && !ctx->tensor_ok)
     return set_error(err, PI_E_CONFIG, "sum factorisation needs p >= 2 and the tensor-product tables");
   if (variant == PI_VARIANT_DENSE && ctx->p > (ctx->n_eq == 3 ? 3 : 2))
@@ -515,7 +542,11 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     constexpr int TG = p1_threads<true>(), TL = p1_threads<false>();
     const unsigned gg = static_cast<unsigned>((n_elem + TG - 1) / TG), gl = static_cast<unsigned>((n_elem + TL - 1) / TL);
-    if (general && fout)
+    if (general && out32)
+      p1_thread_kernel<true, false, float><<<gg, TG, 0, s>>>(a, t);
+    else if (out32)
+      p1_thread_kernel<false, false, float><<<gl, TL, 0, s>>>(a, t);
+    else if (general && fout)
       p1_thread_kernel<true, true><<<gg, TG, 0, s>>>(a, t);
     else if (general)
       p1_thread_kernel<true><<<gg, TG, 0, s>>>(a, t);
@@ -523,6 +554,11 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
       p1_thread_kernel<false, true><<<gl, TL, 0, s>>>(a, t);
     else
       p1_thread_kernel<false><<<gl, TL, 0, s>>>(a, t);
+  } else if (out32 && ctx->variant == PI_VARIANT_TC32 && form != kFormElasticity) {
+    // FP32 output on the tcgen05 tensor cores (3xTF32, kernels_tc32.cuh); opt-in:
+    // measured slower than the FP64 DMMA kernels rounding at the store
+    Tc32Tables t{ctx->d_tc_bhi, ctx->d_tc_blo, ctx->d_tc_xg, ctx->d_tc_y, ctx->d_tri, ctx->d_tc_z, ctx->d_w};
+    tc32_launch(ctx->p, general, a, t, s);
   } else {
     SumFactTables t{ctx->d_xfrag, ctx->d_xplain, ctx->d_yline, ctx->d_tri, ctx->d_w};
     sumfact_launch(ctx->p, ne, form, symmetric, a, t, s);
@@ -562,12 +598,32 @@ pi_status pi_integrate_load(pi_context* ctx, int64_t n_elem, int64_t element_id_
                             int64_t geom_ld, int coeff_mode, const double* coeff, int64_t coeff_ld, double* out,
                             int out_layout, int64_t ld_out, const double* f, double f_const, double* load_out,
                             void* stream, pi_error_info* err) {
-  if ((!out || !load_out) && n_elem > 0) {
-    if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if ((!out || !load_out) && n_elem > 0)
     return set_error(err, PI_E_CONTRACT, "stiffness and load-vector output buffers must be non-NULL");
-  }
-  return integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, out, nullptr,
-                        out_layout, ld_out, stream, err, f, f_const, load_out);
+  if (ctx->n_eq != 1)
+    return set_error(err, PI_E_CONFIG, "load vectors need a scalar weak form (n_eq = 1; context has %d)", ctx->n_eq);
+  // Fused (the stiffness kernel also forms F from its own Jacobians) or a
+  // second, sum-factorised launch on the same stream.  Measured (bench.py
+  // load_vectors): fusing pays where K is cheap (p = 1: the geometry is read
+  // once); at p >= 2 the extra producer work on the stiffness kernel's
+  // critical path costs more (7-21 %) than re-reading 144 B of geometry.
+  const bool fuse = ctx->load_fusion == PI_LOAD_FUSED || (ctx->load_fusion == PI_LOAD_AUTO && ctx->p == 1);
+  if (fuse)
+    return integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, out, nullptr,
+                          out_layout, ld_out, stream, err, f, f_const, load_out);
+  const pi_status st = integrate_impl(ctx, n_elem, element_id_base, geom, geom_ld, coeff_mode, coeff, coeff_ld, out,
+                                      nullptr, out_layout, ld_out, stream, err);
+  if (st != PI_OK || n_elem == 0) return st;
+  return pi_load_vectors(ctx, n_elem, element_id_base, geom, geom_ld, f, f_const, load_out, stream, err);
+}
+
+pi_status pi_context_set_load_fusion(pi_context* ctx, int mode, pi_error_info* err) {
+  if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
+  if (mode < PI_LOAD_AUTO || mode > PI_LOAD_SEPARATE) return set_error(err, PI_E_CONFIG, "unknown load mode %d", mode);
+  ctx->load_fusion = mode;
+  return PI_OK;
 }
 
 pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom,
@@ -592,8 +648,9 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
     const int ns = ctx->n_q / (ctx->p + 1);
     LoadSfTables lt{ctx->d_tri, ctx->d_yline, ctx->d_xplain, ctx->d_w, ns, ctx->p + 1, ctx->p + 1,
                     ctx->n_shape / (ctx->p + 1), ctx->sf_ntps};
-    const size_t smem = sizeof(double) * kLoadSfElems * (21 + ctx->n_q + ns * (ctx->p + 1));
-    const unsigned grid = static_cast<unsigned>((n_elem + kLoadSfElems - 1) / kLoadSfElems);
+    const size_t smem = load_sf_smem(ns, ctx->p + 1);
+    const int epc = load_sf_elems(ns, ctx->p + 1);
+    const unsigned grid = static_cast<unsigned>((n_elem + epc - 1) / epc);
     load_vector_sf_kernel<<<grid, kLoadSfThreads, smem, s>>>(a, lt, f, f_const);
   } else {
     const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);

@@ -1,4 +1,6 @@
-"""Load vectors fused into the stiffness pass (pi_integrate_load).
+"""Load vectors with the stiffness pass (pi_integrate_load),
+fused into every scalar stiffness kernel family (LOAD_FUSED) and as the
+separate sum-factorised launch (LOAD_SEPARATE).
 
 F_i = sum_q det w_q f phi_i(x_q) has no reference entry point;
 it equals f times column 0 of the mass matrix integrate_generic returns for
@@ -43,9 +45,10 @@ def sym_tensor():
 FORMS = ["laplace", "cdr", "symmetric"]
 
 
+@pytest.mark.parametrize("fusion", [pb.LOAD_FUSED, pb.LOAD_SEPARATE])
 @pytest.mark.parametrize("p", range(1, 8))
 @pytest.mark.parametrize("form", FORMS)
-def test_fused_load_vectors(p, form):
+def test_fused_load_vectors(p, form, fusion):
     mesh = pb.generate_box_mesh(5, 3, 3, 0.2, seed=17)
     n = len(mesh) if p <= 4 else (13 if p == 5 else 5)  # ragged: partial CTAs / element groups
     mesh = mesh[:n]
@@ -60,6 +63,7 @@ def test_fused_load_vectors(p, form):
     f = np.linspace(0.5, 2.0, n)
     fd = torch.from_numpy(f).cuda()
     with pb.Integrator(p) as it:
+        it.set_load_fusion(fusion)
         k_plain = torch.full((n, nsh, nsh), float("nan"), dtype=torch.float64, device="cuda")
         it.integrate_device(n, geom, k_plain, mode, coeff)
         k_fused = torch.full_like(k_plain, float("nan"))
@@ -90,6 +94,7 @@ def test_fused_load_vectors_sumfact_variant_and_standalone(p):
     geom = torch.from_numpy(np.ascontiguousarray(mesh.reshape(n, 18).T)).cuda()
     f = torch.linspace(1.0, 3.0, n, dtype=torch.float64, device="cuda")
     with pb.Integrator(p, variant=pb.VARIANT_SUMFACT) as it:
+        it.set_load_fusion(pb.LOAD_FUSED)
         load = torch.full((n, nsh), float("nan"), dtype=torch.float64, device="cuda")
         it.integrate_device(n, geom, torch.empty((n, nsh, nsh), dtype=torch.float64, device="cuda"), pb.LAPLACE,
                             load_out=load, f=f)
@@ -114,6 +119,8 @@ def test_fused_load_vectors_contract():
             it.integrate_device(n, geom, out, pb.ELASTICITY, mats,
                                 load_out=torch.empty((n, it.n_shape), dtype=torch.float64, device="cuda"))
     with pb.Integrator(2) as it:
+        with pytest.raises(pb.ConfigError):
+            it.set_load_fusion(7)
         out32 = torch.empty((n, 18, 18), dtype=torch.float32, device="cuda")
         with pytest.raises(pb.ContractViolation):
             it.integrate_device(n, geom, out32, pb.LAPLACE, load_out=torch.empty((n, 18), dtype=torch.float64,
