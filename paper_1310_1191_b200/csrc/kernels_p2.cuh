@@ -51,6 +51,12 @@ __device__ __forceinline__ const float* p2_phi<float>(const P2Tables& tb) {
 // staged element pitch: 16-byte multiple (TMA bulk stores of whole elements),
 // 2-way bank conflicts at most for the staging writes
 constexpr int kP2Pitch = kP2KK + 2;
+constexpr int kP2Half = 16;  // elements per bulk-store half (symmetric kernel)
+#ifdef PI_P2_ONEHALF  // A/B: one round of 32 element stores (2.5 % slower, Laplace)
+constexpr bool kP2OneHalf = true;
+#else
+constexpr bool kP2OneHalf = false;
+#endif
 
 // GENERAL: full 4x4 tensor (uniform in args.cu, or per element in
 // args.coeff); SYM: the tensor is symmetric, so K is (upper triangle only).
@@ -59,7 +65,6 @@ constexpr int kP2Pitch = kP2KK + 2;
 template <bool GENERAL, bool SYM>
 struct P2Cfg {
   static constexpr int NW = SYM ? 9 : 18;
-  static constexpr int NR = SYM ? 2 : 1;                 // rows per warp
   static constexpr int NACC = SYM ? kP2NSH + 1 : kP2NSH;
   static constexpr int NTHREADS = 32 * NW;
   static constexpr int NM = GENERAL ? 16 : 6;            // stored M entries per point
@@ -84,6 +89,8 @@ struct P2Cfg {
   static constexpr size_t SMEM_BYTES_LOAD = (SMEM_DOUBLES + kP2NQ * 32) * sizeof(double);
   // per-SMSP register file (16K regs; warps dealt round-robin to the 4 SMSPs):
   // 9-warp CTAs x3 need <= 72 registers, one 18-warp CTA <= 96
+  // per-SMSP register file (16K regs; warps dealt round-robin to the 4 SMSPs):
+  // 9-warp CTAs x3 need <= 72 registers, one 18-warp CTA <= 96
   static constexpr int MAXREG = SYM ? 72 : 96;
 };
 
@@ -96,9 +103,19 @@ __device__ __forceinline__ int p2_mslot(int k, int l) {
   return a == 0 ? b : (a == 1 ? 2 + b : 5);
 }
 
-template <int NR, int W>
+// Symmetric tensors: warp w owns the upper-triangle parts of rows w and 17 - w
+// (19 accumulators).  Dealing rows by their per-point cost instead (the
+// busiest warp 48 FMAs per point instead of 53) needs up to 31 accumulators
+// and measured 2.3x slower: the register budget drops the kernel to one CTA
+// per SM.
+__host__ __device__ constexpr int p2_sym_row(int w, int r) { return r == 0 ? w : r == 1 ? 17 - w : -1; }
+template <bool SYM, int W>
+__device__ __forceinline__ constexpr int p2_nr() {
+  return !SYM ? 1 : (p2_sym_row(W, 2) >= 0 ? 3 : p2_sym_row(W, 1) >= 0 ? 2 : 1);
+}
+template <bool SYM, int W>
 __device__ __forceinline__ constexpr int p2_row(int r) {
-  return NR == 1 ? W : (r == 0 ? W : kP2NSH - 1 - W);
+  return SYM ? p2_sym_row(W, r) : W;
 }
 
 // The warp's rows over all rule points.
@@ -106,7 +123,7 @@ template <typename T, bool GENERAL, bool SYM, int W>
 __device__ __forceinline__ void p2_rows(const P2Tables& tb, const T* __restrict__ sM, int lane, T* acc) {
   using BP = BasisPattern<2>;
   using C = P2Cfg<GENERAL, SYM>;
-  constexpr int K0 = GENERAL ? 0 : 1, NR = C::NR, NM = C::NM;
+  constexpr int K0 = GENERAL ? 0 : 1, NR = p2_nr<SYM, W>(), NM = C::NM;
 #pragma unroll 1
   for (int q = 0; q < kP2NQ; ++q) {
     const T* ph = p2_phi<T>(tb) + q * 4 * kP2NSH;
@@ -122,14 +139,14 @@ __device__ __forceinline__ void p2_rows(const P2Tables& tb, const T* __restrict_
     for (int k = K0; k < 4; ++k) {
       bool need = false;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) need = need || BP::nz(k, p2_row<NR, W>(r));
+      for (int r = 0; r < NR; ++r) need = need || BP::nz(k, p2_row<SYM, W>(r));
       if (!need) continue;
       T mk[4];
 #pragma unroll
       for (int l = K0; l < 4; ++l) mk[l] = mq[p2_mslot<GENERAL>(k, l) * 32];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        const int i = p2_row<NR, W>(r);
+        const int i = p2_row<SYM, W>(r);
         if (BP::nz(k, i)) {
           const T f = ph[k * kP2NSH + i];
 #pragma unroll
@@ -140,7 +157,7 @@ __device__ __forceinline__ void p2_rows(const P2Tables& tb, const T* __restrict_
     int off = 0;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      const int i = p2_row<NR, W>(r);
+      const int i = p2_row<SYM, W>(r);
 #pragma unroll
       for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
         T s = acc[off + j - (SYM ? i : 0)];
@@ -186,12 +203,13 @@ __device__ __forceinline__ void p2_row_general(const P2Tables& tb, const T* __re
 }
 
 // Writes the lane's accumulators as rows of its staged element matrix.
-template <bool SYM, int NR, int W, typename T>
+template <bool SYM, int W, typename T>
 __device__ __forceinline__ void p2_stage(T* st, const T* acc) {
+  constexpr int NR = p2_nr<SYM, W>();
   int off = 0;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int i = p2_row<NR, W>(r);
+    const int i = p2_row<SYM, W>(r);
 #pragma unroll
     for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
       const T v = acc[off + j - (SYM ? i : 0)];
@@ -202,12 +220,13 @@ __device__ __forceinline__ void p2_stage(T* st, const T* acc) {
   }
 }
 
-template <bool SYM, int NR, int W, typename T>
+template <bool SYM, int W, typename T>
 __device__ __forceinline__ void p2_store_soa(const LaunchArgs& args, int64_t e, const T* acc) {
+  constexpr int NR = p2_nr<SYM, W>();
   int off = 0;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int i = p2_row<NR, W>(r);
+    const int i = p2_row<SYM, W>(r);
 #pragma unroll
     for (int j = SYM ? i : 0; j < kP2NSH; ++j) {
       const double v = acc[off + j - (SYM ? i : 0)];
@@ -240,7 +259,6 @@ template <bool GENERAL, bool SYM, typename T = double, bool LOAD = false>
 __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const __grid_constant__ LaunchArgs args,
                                                                          const __grid_constant__ P2Tables tb) {
   using C = P2Cfg<GENERAL, SYM>;
-  constexpr int NR = C::NR;
   extern __shared__ __align__(16) double p2_smem[];
   T* sM = reinterpret_cast<T*>(p2_smem);  // M [q][NM][32], then the output staging (same byte size as FP64)
   double* sD = p2_smem + C::OFF_D;
@@ -274,7 +292,15 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
     if (g + gridDim.x < groups) prefetch(g + gridDim.x, buf ^ 1);
     else cp_async_commit();  // keep the group count uniform
     cp_async_wait<1>();      // this group's copies have landed
-    if (bulk && threadIdx.x < 32) bulk_wait_read();  // previous group's element stores no longer read sM
+    // previous group's first-half element stores no longer read sM (M lives in
+    // that half); the second half may still be draining to HBM
+    if (bulk && kP2OneHalf && threadIdx.x < 32) bulk_wait_read();
+    if (bulk && !kP2OneHalf && threadIdx.x < kP2Half) {
+      if constexpr (C::MBUF <= kP2Half * kP2Pitch)
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      else  // general tensors: M (16 entries per point) spans both halves
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
     double* sC = p2_smem + C::OFF_C + buf * 16 * 32;
     if (warp == 0) {
       const double* sx = p2_smem + C::OFF_G + buf * 18 * 32 + lane;
@@ -326,8 +352,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
       static_assert(sizeof(T) == 8, "fused load vectors are FP64");
       if (live) {
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const int i = r == 0 ? warp : kP2NSH - 1 - warp;
+        for (int i = warp; i < kP2NSH; i += C::NW) {  // F rows dealt round-robin over the warps
           double fi = 0.0;
 #pragma unroll
           for (int q = 0; q < kP2NQ; ++q) fi = fma(p2_smem[C::OFF_DW + q * 32 + lane], tb.phi[q * 4 * kP2NSH + i], fi);
@@ -338,7 +363,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
     if (args.out_layout == PI_OUT_SOA) {
       if (live) {
         if constexpr (SYM) {
-#define P2_SOA(W) p2_store_soa<SYM, NR, W>(args, e, acc)
+#define P2_SOA(W) p2_store_soa<SYM, W>(args, e, acc)
           P2_WARP_SWITCH(P2_SOA)
 #undef P2_SOA
         } else {
@@ -348,12 +373,43 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
       }
       continue;
     }
+    if (bulk && !kP2OneHalf) {
+      // Two halves of 16 elements, each one TMA bulk store per element (2592 B,
+      // 16-byte aligned on both sides) issued by threads 0..15 as soon as that
+      // half is staged: the half holding M drains first, so the next group's M
+      // pass waits only for it (about half the former drain wait).
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1) {  // the second half's previous stores (one group ago) are read
+          if (threadIdx.x < kP2Half) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncthreads();
+        }
+        if (lane / kP2Half == h) {
+          T* st = sM + lane * kP2Pitch;
+#define P2_STAGE(W) p2_stage<SYM, W>(st, acc)
+          P2_WARP_SWITCH(P2_STAGE)
+#undef P2_STAGE
+        }
+        const int64_t first = g * 32 + kP2Half * h;
+        const int64_t left = args.n_elem - first;
+        const int n_here = left <= 0 ? 0 : (left < kP2Half ? static_cast<int>(left) : kP2Half);
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x < kP2Half) {
+          if (threadIdx.x < n_here)
+            bulk_store(args.out + (first + threadIdx.x) * kP2KK,
+                       reinterpret_cast<const double*>(sM) + (kP2Half * h + threadIdx.x) * kP2Pitch, kP2KK * 8u);
+          bulk_commit();  // one group per half and issuing thread (empty when n_here is short)
+        }
+      }
+      continue;
+    }
 #pragma unroll 1
     for (int h = 0; h < 32 / C::ROUND; ++h) {
       if (lane / C::ROUND == h) {
         T* st = sM + (lane % C::ROUND) * kP2Pitch;
         if constexpr (SYM) {
-#define P2_STAGE(W) p2_stage<SYM, NR, W>(st, acc)
+#define P2_STAGE(W) p2_stage<SYM, W>(st, acc)
           P2_WARP_SWITCH(P2_STAGE)
 #undef P2_STAGE
         } else {
@@ -364,8 +420,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
       const int64_t first = g * 32 + C::ROUND * h;
       const int64_t left = args.n_elem - first;
       const int n_here = left <= 0 ? 0 : (left < C::ROUND ? static_cast<int>(left) : C::ROUND);
-      if (bulk) {
-        // one TMA bulk store per element (2592 B, 16-byte aligned on both sides)
+      if (bulk) {  // kP2OneHalf
         fence_proxy_async_smem();
         __syncthreads();
         if (threadIdx.x < n_here) {
@@ -373,7 +428,7 @@ __global__ void __maxnreg__((P2Cfg<GENERAL, SYM>::MAXREG)) p2_lane_kernel(const 
                      reinterpret_cast<const double*>(sM) + threadIdx.x * kP2Pitch, kP2KK * 8u);
           bulk_commit();
         }
-        continue;  // the issuing threads wait for the reads before sM is rewritten
+        continue;
       }
       __syncthreads();
       for (int r = threadIdx.x; r < n_here * kP2KK; r += C::NTHREADS) {
