@@ -145,13 +145,13 @@ __device__ __forceinline__ void prism_edges(const double* __restrict__ x, double
 // Jacobian of the multilinear map at xi from the edge vectors (stride DS)
 // and its cofactors cf[i][k] (of J[i][k] = dx_i/dxi_k); returns det.
 // inv[k][i] = cf[i][k] / det (geometry.cpp:60-83).
-template <int DS = 1>
-__device__ __forceinline__ double jacobian_cofactors(const double* __restrict__ dp, double xi1, double xi2,
-                                                     double xi3, double cf[3][3]) {
-  auto d = [dp](int i) { return dp[i * DS]; };
-  const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
-  const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
-  double j[3][3];
+// T: the arithmetic type (double; float for the FP32 variant), edges stored as double.
+template <int DS = 1, typename T = double>
+__device__ __forceinline__ T jacobian_cofactors(const double* __restrict__ dp, T xi1, T xi2, T xi3, T cf[3][3]) {
+  auto d = [dp](int i) { return static_cast<T>(dp[i * DS]); };
+  const T zm = T(0.5) * (T(1) - xi3), zp = T(0.5) * (T(1) + xi3);
+  const T l0 = T(0.5) * (T(1) - xi1 - xi2), l1 = T(0.5) * xi1, l2 = T(0.5) * xi2;
+  T j[3][3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     j[i][0] = fma(zm, d(0 + i), zp * d(3 + i));
@@ -177,26 +177,25 @@ __device__ __forceinline__ double jacobian_cofactors(const double* __restrict__ 
 //            M_k0 = w sum_a c_a-1,k-1 C_a0,
 //            M_kl = (w/det) sum_ab c_a-1,k-1 C_ab c_b-1,l-1.
 // wd = w / det.  CS: element stride of the coefficient array.
-template <bool GENERAL, int CS = 1>
-__device__ __forceinline__ void block_from_cofactors(const double cf[3][3], double det, double w, double wd,
-                                                     const double* cp, double M[16]) {
-  auto c = [cp](int i) { return cp[i * CS]; };
+template <bool GENERAL, int CS = 1, typename T = double>
+__device__ __forceinline__ void block_from_cofactors(const T cf[3][3], T det, T w, T wd, const double* cp, T M[16]) {
+  auto c = [cp](int i) { return static_cast<T>(cp[i * CS]); };
   if (!GENERAL) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
       for (int l = k; l < 3; ++l) {
-        const double v = wd * fma(cf[0][k], cf[0][l], fma(cf[1][k], cf[1][l], cf[2][k] * cf[2][l]));
+        const T v = wd * fma(cf[0][k], cf[0][l], fma(cf[1][k], cf[1][l], cf[2][k] * cf[2][l]));
         M[(k + 1) * 4 + (l + 1)] = v;
         M[(l + 1) * 4 + (k + 1)] = v;
       }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      M[k] = 0.0;
-      M[k * 4] = 0.0;
+      M[k] = T(0);
+      M[k * 4] = T(0);
     }
   } else {
-    double W[4][3];  // W[a][l-1] = sum_b C_ab c_b-1,l-1
+    T W[4][3];  // W[a][l-1] = sum_b C_ab c_b-1,l-1
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -247,12 +246,14 @@ __device__ __forceinline__ void lame(double young, double nu, double& lam, doubl
 // DS / CS: element strides of the edge-vector and coefficient arrays (1 for
 // per-thread arrays; 32 for lane-interleaved shared-memory arrays).
 // Returns det (<= 0 flags an inverted element, geometry.cpp:67-69).
-template <bool GENERAL, int DS = 1, int CS = 1>
-__device__ __forceinline__ double point_block(const double* __restrict__ dp, double xi1, double xi2, double xi3,
-                                              double w, const double* cp, double M[16]) {
-  double cf[3][3];
-  const double det = jacobian_cofactors<DS>(dp, xi1, xi2, xi3, cf);
-  block_from_cofactors<GENERAL, CS>(cf, det, w, w * __drcp_rn(det), cp, M);
+__device__ __forceinline__ double rcp_rn(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ float rcp_rn(float x) { return __frcp_rn(x); }
+template <bool GENERAL, int DS = 1, int CS = 1, typename T = double>
+__device__ __forceinline__ T point_block(const double* __restrict__ dp, T xi1, T xi2, T xi3, T w, const double* cp,
+                                         T M[16]) {
+  T cf[3][3];
+  const T det = jacobian_cofactors<DS, T>(dp, xi1, xi2, xi3, cf);
+  block_from_cofactors<GENERAL, CS, T>(cf, det, w, w * rcp_rn(det), cp, M);
   return det;
 }
 

@@ -57,9 +57,9 @@ struct BasisPattern {
 // skipped at compile time (13 of the 24 phi entries per point are non-zero),
 // so the contraction costs about half the dense loop nest's FMAs.
 // LOAD: also the load vector F_i = sum_q det w_q f phi_0(i, q) (6 more accumulators).
-// T = float: the FP32 arithmetic variant (pi_integrate_f32): Jacobian and
-// point block in FP64, rounded once per point; phi, the accumulation, the
-// staging and the stores in FP32 (half the registers, staging and bytes).
+// T = float: the FP32 arithmetic variant (pi_integrate_f32): Jacobian, point
+// block, phi, the accumulation, the staging and the stores in FP32 (half the
+// registers, staging and output bytes).
 template <bool GENERAL, bool LOAD = false, typename T = double>
 __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MINB_GENERAL : PI_P1_MINB)
     p1_thread_kernel(LaunchArgs args, DenseTables tab) {
@@ -114,12 +114,11 @@ __global__ void __launch_bounds__(p1_threads<GENERAL>(), GENERAL ? 2 * PI_P1_MIN
 
 #pragma unroll 1
   for (int q = 0; q < NQ; ++q) {
-    double Md[16];
-    const double det = point_block<GENERAL>(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2], sW[q], cf, Md);
-    inverted |= !(det > 0.0);
+    // FP32 variant: the Jacobian and point block in FP32 too (det relative error ~1e-7)
     T M[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) M[k] = static_cast<T>(Md[k]);
+    const T det = point_block<GENERAL, 1, 1, T>(d, static_cast<T>(sPts[3 * q]), static_cast<T>(sPts[3 * q + 1]),
+                                                static_cast<T>(sPts[3 * q + 2]), static_cast<T>(sW[q]), cf, M);
+    inverted |= !(det > T(0));
     const T* ph = sPhi + q * 4 * NSH;
     if constexpr (LOAD) {
       const double dwf = det * sW[q] * fe;
