@@ -45,9 +45,23 @@ struct PairsConfig {
   struct Cfg {
     int ppw, ncw, npw;
   };
+#ifndef PI_PAIRS_CFG5
+#define PI_PAIRS_CFG5 1, 7, 3
+#endif
+#ifndef PI_PAIRS_CFG6
+#define PI_PAIRS_CFG6 1, 7, 3
+#endif
   static constexpr Cfg cfg() {
     if (NE == 1 && P == 7) {
       constexpr int v[3] = {PI_PAIRS_CFG7};
+      return {v[0], v[1], v[2]};
+    }
+    if (NE == 1 && P == 6) {
+      constexpr int v[3] = {PI_PAIRS_CFG6};
+      return {v[0], v[1], v[2]};
+    }
+    if (NE == 1 && P == 5) {
+      constexpr int v[3] = {PI_PAIRS_CFG5};
       return {v[0], v[1], v[2]};
     }
     if (NE == 1) return {1, 7, 3};

@@ -101,8 +101,8 @@ template <> struct SumFactLaunch<4, 1> : SumFactLaunchP<PI_SF_4_1> {};
 #define PI_SF_5_1 false, 1, 3, 1, 0, 0, 8, 2, 2, 1, 1
 #endif
 template <> struct SumFactLaunch<5, 1> : SumFactLaunchP<PI_SF_5_1> {};
-#ifndef PI_SF_6_1
-#define PI_SF_6_1 false, 1, 1, 1, 0, 0, 5, 2, 4, 1, 1
+#ifndef PI_SF_6_1  // NB = 3 (9 consumer warps), 3 producer warps: CDR +11 % over NB = 5, NPW = 2
+#define PI_SF_6_1 false, 1, 1, 1, 0, 0, 3, 3, 4, 1, 1
 #endif
 template <> struct SumFactLaunch<6, 1> : SumFactLaunchP<PI_SF_6_1> {};
 #ifndef PI_SF_7_1
