@@ -134,6 +134,25 @@ __device__ __forceinline__ void prism_edges(const double* __restrict__ x, double
   }
 }
 
+// det J only (load vectors): three cofactors instead of nine.
+template <int DS = 1>
+__device__ __forceinline__ double jacobian_det(const double* __restrict__ dp, double xi1, double xi2, double xi3) {
+  auto d = [dp](int i) { return dp[i * DS]; };
+  const double zm = 0.5 * (1.0 - xi3), zp = 0.5 * (1.0 + xi3);
+  const double l0 = 0.5 * (1.0 - xi1 - xi2), l1 = 0.5 * xi1, l2 = 0.5 * xi2;
+  double j[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    j[i][0] = fma(zm, d(0 + i), zp * d(3 + i));
+    j[i][1] = fma(zm, d(6 + i), zp * d(9 + i));
+    j[i][2] = fma(l0, d(12 + i), fma(l1, d(15 + i), l2 * d(18 + i)));
+  }
+  const double c0 = j[1][1] * j[2][2] - j[1][2] * j[2][1];
+  const double c1 = j[1][2] * j[2][0] - j[1][0] * j[2][2];
+  const double c2 = j[1][0] * j[2][1] - j[1][1] * j[2][0];
+  return j[0][0] * c0 + j[0][1] * c1 + j[0][2] * c2;
+}
+
 // The per-point block M = T (det w C) T^T of coefficient_block, built from
 // the cofactors c_ik of J without forming J^-1 (inv[k][i] = c_ik / det,
 // geometry.cpp:60-83):

@@ -327,8 +327,7 @@ __global__ void __launch_bounds__(kLoadSfThreads)
     double u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool inverted = false;
     for (int z = 0; z < nz; ++z) {
-      double cf[3][3];
-      const double det = jacobian_cofactors(d, xi1, xi2, __ldg(tb.yline + 2 * nv * nz + z), cf);
+      const double det = jacobian_det(d, xi1, xi2, __ldg(tb.yline + 2 * nv * nz + z));
       inverted |= !(det > 0.0);
       const double dw = det * __ldg(tb.w + z * ns + s) * fe;
 #pragma unroll
@@ -341,12 +340,21 @@ __global__ void __launch_bounds__(kLoadSfThreads)
       if (a < nv) sU[(el * ns + s) * nv + a] = u[a];
   }
   __syncthreads();
-  for (int i = tid; i < ne * nsh; i += kLoadSfThreads) {
-    const int el = i / nsh, dof = i - el * nsh, t = dof / nv, a = dof - t * nv;
-    const double* u = sU + el * ns * nv + a;
-    double acc = 0.0;
-    for (int s = 0; s < ns; ++s) acc = fma(__ldg(tb.xplain + (s * 3 + 2) * tb.ntps + t), u[s * nv], acc);
-    args.out[(e0 + el) * nsh + dof] = acc;
+  // thread = (element, t): the nv values F(t, .) share each X_2(t, s) load
+  for (int i = tid; i < ne * nt; i += kLoadSfThreads) {
+    const int el = i / nt, t = i - el * nt;
+    const double* u = sU + el * ns * nv;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int s = 0; s < ns; ++s) {
+      const double x2 = __ldg(tb.xplain + (s * 3 + 2) * tb.ntps + t);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (a < nv) acc[a] = fma(x2, u[s * nv + a], acc[a]);
+    }
+    double* dst = args.out + (e0 + el) * nsh + t * nv;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+      if (a < nv) dst[a] = acc[a];
   }
 }
 
