@@ -78,7 +78,12 @@ struct PairsConfig {
   static constexpr int NBUF = P == 7 ? PI_PAIRS_NBUF7 : PI_PAIRS_NBUF;
   // M: all points of the element (scalar forms), double buffered across items
   static constexpr bool MALL = NE == 1;
-  static constexpr int MITEMS = (MALL ? NSP : 4) * NZ;
+#ifdef PI_SF_MS_EVEN
+  static constexpr int MS = NZ;
+#else
+  static constexpr int MS = NZ | 1;  // odd point stride per s (kernels_sumfact.cuh MS)
+#endif
+  static constexpr int MITEMS = (MALL ? NSP : 4) * MS;
   static constexpr int MPITCH = MITEMS | 1;
   static constexpr int M_PER_BUF = NE * NE * 16 * MPITCH;
   static constexpr int OFF_XA = 0;
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
       double* sMb = sM + buf * C::M_PER_BUF;
       for (int i = ptid; i < s_count * NZ; i += C::NPT) {
         const int z = i % NZ, s = s_first + i / NZ;
-        double* Mi = sMb + i;
+        double* Mi = sMb + (i / NZ) * C::MS + z;
         if (s < NS) {
           double cf[3][3];
           const double det = jacobian_cofactors(sGeom, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(PairsConfig<P, NE>::NTHREADS, 1)
             const int a = ap / NE, ie = ap % NE, b = bp / NE, je = bp % NE;
             const int kx = x < 2 ? x + 1 : 3;
             const int s_row = C::MALL ? chunk * 4 + sl : sl;
-            const double* Mp = sM + mb * C::M_PER_BUF + s_row * NZ + ((ie * NE + je) * 16) * C::MPITCH;
+            const double* Mp = sM + mb * C::M_PER_BUF + s_row * C::MS + ((ie * NE + je) * 16) * C::MPITCH;
 #pragma unroll
             for (int z = 0; z < NZ; ++z) {
               auto M = [Mp, z](int k) { return Mp[k * C::MPITCH + z]; };

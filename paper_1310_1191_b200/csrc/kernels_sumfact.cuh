@@ -326,10 +326,18 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR
   // latency-bound pass instead of one per chunk); systems (9 blocks per
   // point) build it per chunk of 4 triangle points.
   static constexpr bool MALL = NE == 1;
-  // M stored k-major: [NE*NE][16][MPITCH], point (el, s, z) at el*MEL + s*NZ + z
+  // M stored k-major: [NE*NE][16][MPITCH], point (el, s, z) at el*MEL + s*MS + z
   // (an odd k-row pitch; padding MEL / MPITCH against the producers' read
   // conflicts measured no gain).
-  static constexpr int MEL = (MALL ? S::NSP : 4) * S::NZ;  // points per element per M pass
+  // point stride per triangle point s: NZ made odd, so the producers' reads of
+  // one M row at different (x, s) fall into distinct banks (k-row offsets are
+  // multiples of 4 doubles, s offsets then are not)
+#ifdef PI_SF_MS_EVEN  // A/B: the former stride NZ
+  static constexpr int MS = S::NZ;
+#else
+  static constexpr int MS = S::NZ | 1;
+#endif
+  static constexpr int MEL = (MALL ? S::NSP : 4) * MS;  // point slots per element per M pass
   static constexpr int MPITCH = (L::EPC * MEL) | 1;
   static constexpr int M_PER_CHUNK = NE * NE * 16 * MPITCH;
   static constexpr int NCOEF = 16 * NE * NE;            // coefficient tensor per element
@@ -523,7 +531,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
       for (int i = ptid; i < EPC * s_count * NZ; i += C::NPT) {
         const int z = i % NZ, sl = (i / NZ) % s_count, el = i / (s_count * NZ);
         const int s = s_first + sl;
-        double* Mi = sMb + el * C::MEL + sl * NZ + z;
+        double* Mi = sMb + el * C::MEL + sl * C::MS + z;
         if (s < NS) {
           double cf[3][3];
           const double det = jacobian_cofactors(sGeom + 21 * el, sTri[s], sTri[NS + s], sY[2 * NV * NZ + z], cf);
@@ -581,7 +589,7 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
 #pragma unroll
           for (int bb = 0; bb < C::BPER; ++bb) h[bb][0] = h[bb][1] = h[bb][2] = 0.0;
           // M_k of point z at Mp[k*MPITCH + z]
-          const double* Mp = sM + mb * C::M_PER_CHUNK + el * C::MEL + (C::MALL ? chunk * 4 + sl : sl) * NZ;
+          const double* Mp = sM + mb * C::M_PER_CHUNK + el * C::MEL + (C::MALL ? chunk * 4 + sl : sl) * C::MS;
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const double* Mz = Mp + z;
