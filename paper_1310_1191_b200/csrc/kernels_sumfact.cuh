@@ -228,6 +228,16 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR
   // warp reads per k-step land in disjoint bank halves.
   static constexpr int NTPS = (NTP + 7) / 16 * 16 + 8;
   static constexpr int XPLAIN = S::NSP * 3 * NTPS;
+  // natural order: X also as [s][t'][4] (y = 0, 1 in one 16-byte load, y = 2
+  // in an 8-byte one) after the [s][y][t'] table (A/B: PI_SF_NO_XP4)
+#ifdef PI_SF_NO_XP4
+  static constexpr bool XP4 = false;
+#else
+  static constexpr bool XP4 = !L::TMAJOR && S::NV <= 4;  // p <= 3: the table grows as N_s N_t
+#endif
+  static constexpr int XP4_DOUBLES = XP4 ? S::NSP * NTP * 4 : 0;
+  static constexpr int XPLAIN_TOTAL = XPLAIN + XP4_DOUBLES;       // the device table holds both
+  static constexpr int XP_SMEM = XP4 ? XP4_DOUBLES : XPLAIN;     // the consumers stage only the one they read
   static constexpr int NBLK = NTILE / (L::NB * L::NCB);  // n-tile blocks (warps) per CTA and row group
   static constexpr int WPE = (L::AG / L::WA) * NBLK;      // consumer warps per element
   // t'-major warps own whole K rows (all t'-groups, all b), so they stage
@@ -344,7 +354,7 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR
   // shared memory layout (doubles; every block 16-byte aligned)
   static constexpr int OFF_XA = 0;
   static constexpr int OFF_XP = OFF_XA + S::XFRAG;
-  static constexpr int OFF_H = OFF_XP + XPLAIN;
+  static constexpr int OFF_H = OFF_XP + XP_SMEM;
   static constexpr int OFF_M = OFF_H + NBUF * H_PER_BUF;
   static constexpr int OFF_GEOM = OFF_M + (MALL ? 2 : 1) * M_PER_CHUNK;
   static constexpr int OFF_C = OFF_GEOM + (L::EPC * 21 + 1) / 2 * 2;
@@ -377,7 +387,8 @@ struct SumFactConfig : SumFactShape<P, NE, SumFactLaunchSel<P, NE, SYMV>::TMAJOR
 //     F(t, a) = sum_s X_2(t, s) u(s, a),   u(s, a) = sum_z P_a(z) dw(s, z)
 // from dw = det w f per point (sDW [ne][NSP][NZ], zero at padded s); one
 // contiguous coalesced store of N_sh doubles per element.
-template <int NS, int NSP, int NZ, int NV, int NT, int NTPS>
+// X_2(t, s) in shared memory: [s][y][t'] with pitch NTPS, or (XP4 > 0) [s][t'][4] with XP4 = NTP rows
+template <int NS, int NSP, int NZ, int NV, int NT, int NTPS, int XP4 = 0>
 __device__ __forceinline__ void sumfact_load_vectors(const LaunchArgs& args, int64_t e0, int ne, const double* sDW,
                                                      double* sU, const double* sXP, const double2* PD, int ptid,
                                                      int npt, int bar) {
@@ -397,7 +408,8 @@ __device__ __forceinline__ void sumfact_load_vectors(const LaunchArgs& args, int
     const double* u = sU + el * NSP * NV + a;
     double acc = 0.0;
 #pragma unroll 4
-    for (int s = 0; s < NS; ++s) acc = fma(sXP[(s * 3 + 2) * NTPS + t], u[s * NV], acc);
+    for (int s = 0; s < NS; ++s)
+      acc = fma(XP4 ? sXP[(s * XP4 + t) * 4 + 2] : sXP[(s * 3 + 2) * NTPS + t], u[s * NV], acc);
     args.fout[(e0 + el) * NSH + dof] = acc;
   }
 }
@@ -464,11 +476,11 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
   if (tid == 0) mbar_init(&s_tables, 1);
   __syncthreads();
   if (tid == 0) {
-    constexpr unsigned BX = 8u * C::XFRAG, BP = 8u * C::XPLAIN, BY = 8u * ((2 * NV * NZ + NZ + 1) / 2 * 2),
+    constexpr unsigned BX = 8u * C::XFRAG, BP = 8u * C::XP_SMEM, BY = 8u * ((2 * NV * NZ + NZ + 1) / 2 * 2),
                        BT = 8u * 2 * NS, BW = 8u * ((NQ + 1) / 2 * 2);
     mbar_arrive_expect_tx(&s_tables, BX + BP + BY + BT + BW);
     bulk_load(sXA, tab.xfrag, BX, &s_tables);
-    bulk_load(sXP, tab.xplain, BP, &s_tables);
+    bulk_load(sXP, tab.xplain + (C::XP4 ? C::XPLAIN : 0), BP, &s_tables);
     bulk_load(sY, tab.yline, BY, &s_tables);
     bulk_load(sTri, tab.tri, BT, &s_tables);
     bulk_load(sW, tab.w, BW, &s_tables);
@@ -559,7 +571,8 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
       }
       named_sync(kBarProd, C::NPT);
       if (NE == 1 && C::MALL && args.fout && flagger) {
-        sumfact_load_vectors<NS, C::NSP, NZ, NV, NT, C::NTPS>(args, e0, EPC, smem + C::OFF_LDW, smem + C::OFF_LU, sXP,
+        sumfact_load_vectors<NS, C::NSP, NZ, NV, NT, C::NTPS, C::XP4 ? C::NTP : 0>(args, e0, EPC, smem + C::OFF_LDW,
+                                                                                 smem + C::OFF_LU, sXP,
                                                             PD, ptid, C::NPT, kBarProd);
         named_sync(kBarProd, C::NPT);
       }
@@ -828,10 +841,18 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
           if constexpr (WA > 1) {
 #pragma unroll
             for (int nb = 0; nb < NB; ++nb) {
-              const double* xp = Xs + xoff[nb];
-              xr[nb][0] = xp[0];
-              xr[nb][1] = xp[NTPS];
-              xr[nb][2] = xp[2 * NTPS];
+              if constexpr (C::XP4) {
+                const double* xq = sXP + (s * C::NTP + xoff[nb]) * 4;
+                const double2 x01 = *reinterpret_cast<const double2*>(xq);
+                xr[nb][0] = x01.x;
+                xr[nb][1] = x01.y;
+                xr[nb][2] = xq[2];
+              } else {
+                const double* xp = Xs + xoff[nb];
+                xr[nb][0] = xp[0];
+                xr[nb][1] = xp[NTPS];
+                xr[nb][2] = xp[2 * NTPS];
+              }
             }
           }
 #pragma unroll
@@ -852,6 +873,10 @@ __global__ void __launch_bounds__(SumFactConfig<P, NE, SYM>::NTHREADS, SumFactCo
               double gv;
               if constexpr (WA > 1) {
                 gv = fma(h[0], xr[nb][0], fma(h[1], xr[nb][1], h[2] * xr[nb][2]));
+              } else if constexpr (C::XP4) {
+                const double* xq = sXP + (s * C::NTP + xoff[nb]) * 4;
+                const double2 x01 = *reinterpret_cast<const double2*>(xq);
+                gv = fma(h[0], x01.x, fma(h[1], x01.y, h[2] * xq[2]));
               } else {
                 const double* xp = Xs + xoff[nb];
                 gv = fma(h[0], xp[0], fma(h[1], xp[NTPS], h[2] * xp[2 * NTPS]));

@@ -40,7 +40,8 @@ template <int P, int NE>
 struct SumFactHost {
   using C = SumFactConfig<P, NE>;         // tables; the general-form kernels
   using CS = SumFactConfig<P, NE, true>;  // the symmetric-form kernels
-  static_assert(C::TMAJOR == CS::TMAJOR && C::XPLAIN == CS::XPLAIN && C::XFRAG == CS::XFRAG,
+  static_assert(C::TMAJOR == CS::TMAJOR && C::XPLAIN == CS::XPLAIN && C::XPLAIN_TOTAL == CS::XPLAIN_TOTAL &&
+                    C::XFRAG == CS::XFRAG,
                 "both launch shapes of a (p, n_eq) read the same tables");
   template <bool SYM>
   using CK = SumFactConfig<P, NE, SYM>;
@@ -167,12 +168,14 @@ struct SumFactHost {
           if (t < NT && s < NS) v = X[(x * NT + t) * NS + s];
           out.xfrag[(mt * C::KSTEPS + ks) * 32 + lane] = v;
         }
-    out.xplain.assign(C::XPLAIN, 0.0);
+    out.xplain.assign(C::XPLAIN_TOTAL, 0.0);
     out.ntps = C::NTPS;
     for (int s = 0; s < NS; ++s)
       for (int t = 0; t < NT; ++t)
-        for (int x = 0; x < 3; ++x)
+        for (int x = 0; x < 3; ++x) {
           out.xplain[(static_cast<size_t>(s) * 3 + x) * C::NTPS + t] = X[(x * NT + t) * NS + s];
+          if (C::XP4) out.xplain[C::XPLAIN + (static_cast<size_t>(s) * C::NTP + t) * 4 + x] = X[(x * NT + t) * NS + s];
+        }
     return true;
   }
 
