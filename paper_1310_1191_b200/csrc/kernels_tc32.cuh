@@ -47,6 +47,7 @@ struct Tc32Shape {
   // the streams of co-resident CTAs overlap: small CTAs, several per SM.
   static constexpr int CTAS = P <= 4 ? 4 : 1;
   static constexpr int NTHREADS = P <= 4 ? 128 : 256;
+  static constexpr int NISSUE = 4;  // MMA-issuing threads per CTA (lane 0 of warps 0..3)
   // A ring: (a, m-tile, x) units, hi + lo tiles each
   static constexpr int NAB = 2;
   // TMEM: a ring of D slots, one per Legendre row a (MTJ x NPAD columns each);
@@ -349,7 +350,11 @@ __global__ void __launch_bounds__(Tc32Shape<P>::NTHREADS, Tc32Shape<P>::CTAS) su
           }
           fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar_full[buf])) : "memory");
-          if (tid == 0) {
+          // one issuing thread per row a, dealt round-robin over the first warps:
+          // each thread's tcgen05.mma stream completes one MMA per ~150 cycles, and
+          // streams of different threads overlap (tools/microbench/tc_mma_rate.cu);
+          // the MMAs of one D slot stay in one stream, in order
+          if (lane == 0 && warp == static_cast<int>(arow % C::NISSUE)) {
             mbar_wait(&bar_full[buf], (full_ph >> buf) & 1u);
             tc_fence_after();
             const uint32_t d = tmem + slot * C::SLOTC + mt * NPAD;

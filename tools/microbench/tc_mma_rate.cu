@@ -14,7 +14,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t a, uint32_t lbo, uint32_t sbo)
 }
 
 template <int N, int M>
-__global__ void bench(int iters, int nacc, unsigned long long* out) {
+__global__ void bench(int iters, int nacc, unsigned long long* out, int nis = 1) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tm;
@@ -25,7 +25,7 @@ __global__ void bench(int iters, int nacc, unsigned long long* out) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&bar)), "r"(nis));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("fence.proxy.async.shared::cta;");
@@ -33,20 +33,20 @@ __global__ void bench(int iters, int nacc, unsigned long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t d0 = tm;
-  if (tid == 0) {
+  if ((tid & 31) == 0 && (tid >> 5) < nis) {
     const uint32_t sa = su32(sm), sb = sa + 128 * 8 * 4;
     const uint64_t ad = desc(sa, 128 * 16, 128), bd = desc(sb, N * 16, 128);
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t(N) >> 3) << 17) | ((uint32_t(M) >> 4) << 24);
     const long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      const uint32_t d = d0 + (i % nacc) * N;
+      const uint32_t d = d0 + ((tid >> 5) * nacc + (i % nacc)) * N;
       asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
                    ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(i >= nacc ? 1 : 0));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
     asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra W;\n}\n" ::"r"(su32(&bar)));
     const long long t1 = clock64();
-    if (blockIdx.x == 0) out[0] = t1 - t0;
+    if (blockIdx.x == 0 && tid == 0) out[0] = t1 - t0;
   }
   __syncthreads();
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(d0));
@@ -78,6 +78,17 @@ int main() {
     run<16, 64>(d, c);
     run<64, 64>(d, c);
     run<256, 64>(d, c);
+  }
+  // several issuing warps in one CTA, each into its own accumulator
+  for (int nis : {2, 4}) {
+    const int smem = (128 * 8 + 64 * 8) * 4 + 1024;
+    cudaFuncSetAttribute(bench<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench<64, 64><<<148, 128, smem>>>(4096, 1, d, nis);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    printf("M=64 N=64 issuers/CTA=%d: %.1f cycles per MMA of one issuer (%s)\n", nis, double(c) / 4096,
+           cudaGetErrorString(e));
   }
   return 0;
 }
