@@ -547,6 +547,8 @@ def main_ours(args, ws, rank, local):
 
     # ---------------- roofline inputs ----------------
     dmma_tf, dfma_tf = pb.measure_fp64_peak(dev_idx)
+    sm_clock_ghz = (clk.get("sm_mhz") or 1965.0) / 1e3
+    fp32_peak_tf = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * sm_clock_ghz / 1e3
     hbm_peak, hbm_src = peaks_hbm()
 
     def fractions(p, frm, ms):
@@ -558,13 +560,18 @@ def main_ours(args, ws, rank, local):
         ex = f_exec * E / t / 1e12
         hb = byts * E / t / 1e9
         dense_bound_s = max(f_dense * E / (dmma_tf * 1e12), byts * E / (hbm_peak * 1e9))
-        fe, fh = ex / dmma_tf, hb / hbm_peak
+        # the FP32 variant's p <= 2 scalar kernels compute on the FP32 pipe: their
+        # executed FLOPs against the nominal FP32 FMA peak (128 lanes x 2 x SM clock)
+        fp32_arith = R.esz == 4 and p <= 2 and n_eq_f == 1
+        pipe_peak = fp32_peak_tf if fp32_arith else dmma_tf
+        fe, fh = ex / pipe_peak, hb / hbm_peak
+        pipe = "fp32" if fp32_arith else "fp64"
         return {
             "elements_per_s": E / t, "ms": ms, "launches": -(-E // R.chunk(p, frm)),
             "dense_flop_alg_per_element": f_dense, "executed_flop_per_element": f_exec, "bytes_per_element": byts,
             "executed_tflops": ex, "hbm_gbs": hb, "dense_tflops": f_dense * E / t / 1e12,
-            "frac_executed_fp64": fe, "frac_hbm": hb / hbm_peak,
-            "binding": "fp64" if fe >= fh else "hbm", "frac": max(fe, fh),
+            f"frac_executed_{pipe}": fe, "frac_hbm": hb / hbm_peak,
+            "binding": pipe if fe >= fh else "hbm", "frac": max(fe, fh),
             "dense_roofline_elements_per_s": E / dense_bound_s, "frac_of_dense_roofline": dense_bound_s / t,
         }
 
@@ -704,7 +711,7 @@ def main_ours(args, ws, rank, local):
     d = per_p[str(dom)]
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
+    if tf.exists() and R.esz == 8:  # the committed DRAM measurements are of the FP64 kernels
         try:
             per_el = json.load(open(tf)).get(f"p{dom}_{form}")
             traffic = per_el * R.chunk(dom, form) if per_el is not None else None
@@ -714,11 +721,12 @@ def main_ours(args, ws, rank, local):
     kname = {(1, 1): "p1_thread_kernel", (2, 1): "p2_lane_kernel", (1, 3): "p1_elastic_lane_kernel",
              (2, 3): "p2_elastic_warp_kernel", (3, 3): "p3_elastic_cta_kernel"}.get(
         (dom, n_eq), f"sumfact_kernel<{dom}, n_eq={n_eq}> (FP64 DMMA)")
-    fp64_binds = d["binding"] == "fp64"
+    fp64_binds = d["binding"] in ("fp64", "fp32")
+    fp32_dom = "frac_executed_fp32" in d
     roofline = {
         "bound": "tensor" if fp64_binds else "hbm", "kernel": kname,
         "achieved": d["executed_tflops"] if fp64_binds else d["hbm_gbs"],
-        "peak": dmma_tf if fp64_binds else hbm_peak,
+        "peak": (fp32_peak_tf if fp32_dom else dmma_tf) if fp64_binds else hbm_peak,
         "unit": "TFLOP/s" if fp64_binds else "GB/s",
         "frac": d["frac"],
         "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu dram__bytes_read+write, profiles/traffic.json)",
@@ -727,8 +735,11 @@ def main_ours(args, ws, rank, local):
                  "pi_flops_executed_per_element, checked against ncu pipe counters) per launch / launch time, "
                  "against the FP64 pipe peak measured in-run (DMMA m8n8k4; DMMA and DFMA share one FP64 pipe), "
                  "or HBM bytes against the measured copy bandwidth -- whichever is the larger fraction"),
-        "fp64": {"executed_tflops": d["executed_tflops"], "peak_tflops": dmma_tf, "frac": d["frac_executed_fp64"],
-                 "peak_source": f"DMMA m8n8k4 measured in-run (DFMA {dfma_tf:.1f} TF/s)"},
+        ("fp32" if fp32_dom else "fp64"): (
+            {"executed_tflops": d["executed_tflops"], "peak_tflops": fp32_peak_tf, "frac": d["frac_executed_fp32"],
+             "peak_source": "nominal FP32 FMA peak: SMs x 128 lanes x 2 x median SM clock"} if fp32_dom else
+            {"executed_tflops": d["executed_tflops"], "peak_tflops": dmma_tf, "frac": d["frac_executed_fp64"],
+             "peak_source": f"DMMA m8n8k4 measured in-run (DFMA {dfma_tf:.1f} TF/s)"}),
         "hbm": {"gbs": d["hbm_gbs"], "peak_gbs": hbm_peak, "frac": d["frac_hbm"], "peak_source": hbm_src},
         "dense_count": {"tflops": d["dense_tflops"], "frac_of_fp64_peak": d["dense_tflops"] / dmma_tf,
                         "note": "SURVEY 8(d) dense FLOP_alg (no symmetry / sum-factorisation credit); the kernels "
