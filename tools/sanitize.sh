@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 OUT=gpurun_out/sanitize
 mkdir -p $OUT
-FAMS=${FAMS:-p1 p2 sumfact pairs dense elastic load fused initprobe host}
+FAMS=${FAMS:-p1 p2 sumfact pairs dense elastic load fused tc32 initprobe host}
 TOOLS=${TOOLS:-memcheck racecheck synccheck initcheck}
 for tool in $TOOLS; do
   for fam in $FAMS; do

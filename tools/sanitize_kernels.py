@@ -13,6 +13,7 @@ Families (the launch each one reaches, pi_context.cu dispatch):
   elastic  p1_elastic_lane / p2_elastic_warp / p3_elastic_cta, sumfact_kernel<P, 3> p = 4..7
   load     load_vector_kernel p = 1..7
   fused    pi_integrate_load: the scalar kernels with the fused load vector
+  tc32     sumfact_tc32_kernel (tcgen05, TMEM, mbarrier ring), VARIANT_TC32
   initprobe  initcheck and TMA bulk stores (see fam_initprobe)
   host     pi_integrate_host: aos_to_soa_kernel + chunked two-stream path
 """
@@ -123,6 +124,12 @@ def fam_fused():  # pi_integrate_load: every scalar kernel family with the load 
         run(p, n, pb.LAPLACE, load=True)
         run(p, n, pb.PER_ELEMENT, load=True)
     run(2, 40, pb.LAPLACE, variant=pb.VARIANT_SUMFACT, load=True)
+
+
+def fam_tc32():  # sumfact_tc32_kernel (tcgen05 FP32, opt-in VARIANT_TC32)
+    for p in (3, 4, 5):
+        run(p, 5, pb.LAPLACE, variant=pb.VARIANT_TC32, f32=True)
+        run(p, 5, pb.PER_ELEMENT, variant=pb.VARIANT_TC32, f32=True)
 
 
 def fam_initprobe():
