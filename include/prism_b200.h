@@ -180,6 +180,13 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
                             const double* geom_aos, int coeff_mode, const double* coeff, double* out,
                             int64_t chunk_elems, pi_error_info* err);
 
+/* pi_integrate_host plus the load vectors (scalar weak forms; see
+ * pi_integrate_load): f host [n_elem] per-element values or NULL (f_const);
+ * load_out host [n_elem][n_shape]. */
+pi_status pi_integrate_host_load(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
+                                 int coeff_mode, const double* coeff, const double* f, double f_const, double* out,
+                                 double* load_out, int64_t chunk_elems, pi_error_info* err);
+
 /* ---- stiffness containers (host I/O) ---- */
 enum {
   PI_STIFFNESS_PRISTIF1 = 1, /* the reference's single-element f32 container: save_stiffness /

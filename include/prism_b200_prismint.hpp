@@ -124,22 +124,59 @@ class Context {
                element_id_base);
   }
 
+  /// Stiffness matrices and load vectors F_i = sum_q det w_q f phi_i(x_q)
+  /// (scalar weak forms) in one pass over the mesh: f one value per element,
+  /// or empty for f_const everywhere (pi_integrate_host_load).
+  struct WithLoad {
+    std::vector<prismint::ElementStiffness> stiffness;
+    std::vector<std::vector<double>> load;
+  };
+  WithLoad integrate_with_load(std::span<const prismint::PrismGeometry> mesh,
+                               std::span<const prismint::CoefficientTensor> coeffs, std::span<const double> f = {},
+                               double f_const = 1.0, std::int64_t element_id_base = 0) {
+    if (n_eq_ != 1) throw prismint::ConfigError("prism_b200: load vectors need a scalar (n_eq = 1) context");
+    if (coeffs.empty() || (coeffs.size() != 1 && coeffs.size() != mesh.size()))
+      throw prismint::ConfigError("prism_b200: need one coefficient tensor or one per element");
+    if (!f.empty() && f.size() != mesh.size()) throw prismint::ConfigError("prism_b200: need one f per element");
+    std::vector<double> cbuf(coeffs.size() * 16);
+    for (std::size_t k = 0; k < coeffs.size(); ++k) std::memcpy(&cbuf[k * 16], coeffs[k].entries.data(), 16 * 8);
+    const std::size_t n = mesh.size(), kk = static_cast<std::size_t>(nsh_) * nsh_;
+    std::vector<double> geom = flat_geometry(mesh), out(kk * n), load(static_cast<std::size_t>(nsh_) * n);
+    pi_error_info e{};
+    check(pi_integrate_host_load(ctx_, static_cast<std::int64_t>(n), element_id_base, geom.data(),
+                                 coeffs.size() == 1 ? PI_COEFF_UNIFORM : PI_COEFF_PER_ELEMENT, cbuf.data(),
+                                 f.empty() ? nullptr : f.data(), f_const, out.data(), load.data(), 0, &e),
+          e);
+    WithLoad r;
+    r.stiffness = wrap(out, n, kk);
+    r.load.resize(n);
+    for (std::size_t i = 0; i < n; ++i) r.load[i].assign(load.begin() + i * nsh_, load.begin() + (i + 1) * nsh_);
+    return r;
+  }
+
   pi_context* raw() { return ctx_; }
 
  private:
+  static std::vector<double> flat_geometry(std::span<const prismint::PrismGeometry> mesh) {
+    std::vector<double> geom(18 * mesh.size());
+    for (std::size_t e = 0; e < mesh.size(); ++e)
+      for (int v = 0; v < 6; ++v)
+        for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
+    return geom;
+  }
   std::vector<prismint::ElementStiffness> run(std::span<const prismint::PrismGeometry> mesh, int mode,
                                               const double* coeff, std::int64_t element_id_base) {
     const std::size_t n = mesh.size();
-    std::vector<double> geom(18 * n);
-    for (std::size_t e = 0; e < n; ++e)
-      for (int v = 0; v < 6; ++v)
-        for (int c = 0; c < 3; ++c) geom[18 * e + 3 * v + c] = mesh[e].vertices[v][c];
+    std::vector<double> geom = flat_geometry(mesh);
     const std::size_t kk = static_cast<std::size_t>(nsh_) * n_eq_ * nsh_ * n_eq_;
     std::vector<double> out(kk * n);
     pi_error_info e{};
     check(pi_integrate_host(ctx_, static_cast<std::int64_t>(n), element_id_base, geom.data(), mode, coeff,
                             out.data(), 0, &e),
           e);
+    return wrap(out, n, kk);
+  }
+  std::vector<prismint::ElementStiffness> wrap(const std::vector<double>& out, std::size_t n, std::size_t kk) {
     std::vector<prismint::ElementStiffness> res(n);
     for (std::size_t i = 0; i < n; ++i) {
       auto& a = res[i];

@@ -148,6 +148,8 @@ def library():
     L.pi_load_vectors.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, vp, C.c_double, vp, vp, E]
     L.pi_check.argtypes = [vp, E]
     L.pi_integrate_host.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int, vp, vp, C.c_int64, E]
+    L.pi_integrate_host_load.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int, vp, vp, C.c_double, vp, vp,
+                                         C.c_int64, E]
     L.pi_flops_dense_per_element.argtypes = [C.c_int, C.c_int, C.c_int]
     L.pi_flops_dense_per_element.restype = C.c_double
     L.pi_flops_executed_per_element.argtypes = [vp, C.c_int]
@@ -474,6 +476,22 @@ class Integrator:
         _raise(library().pi_check(self._h, C.byref(err)), err)
 
     # -- host buffers: the run_batch-style drop-in --
+    def integrate_host_load(self, geoms, coeff_mode=LAPLACE, coeff=None, f=None, f_const=1.0, element_id_base=0,
+                            chunk_elems=0):
+        """pi_integrate_host_load: host [n][6][3] in, (K [n][dim][dim], F [n][n_shape]) out."""
+        geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
+        n = len(geoms)
+        out = np.empty((n, self.dim, self.dim))
+        load = np.empty((n, self.n_shape))
+        cbuf = _host_coeff(self, coeff_mode, coeff, n)
+        fbuf = None if f is None else np.ascontiguousarray(f, dtype=np.float64).reshape(n)
+        err = _ErrInfo()
+        st = library().pi_integrate_host_load(self._h, n, element_id_base, _addr(geoms), coeff_mode, _addr(cbuf),
+                                              _addr(fbuf), float(f_const), _addr(out), _addr(load), chunk_elems,
+                                              C.byref(err))
+        _raise(st, err)
+        return out, load
+
     def integrate_host(self, geoms, coeff_mode=LAPLACE, coeff=None, element_id_base=0, out=None, chunk_elems=0):
         """geoms: host [n][6][3]; returns host [n][dim][dim] (canonical)."""
         geoms = np.ascontiguousarray(geoms, dtype=np.float64).reshape(-1, 18)
@@ -498,6 +516,14 @@ class Integrator:
                                          _addr(out), chunk_elems, C.byref(err))
         _raise(st, err)
         return out
+
+
+def _host_coeff(it, coeff_mode, coeff, n):
+    if coeff_mode in (UNIFORM, ELASTICITY_UNIFORM):
+        return np.ascontiguousarray(coeff, dtype=np.float64).reshape(-1)
+    if coeff_mode in (PER_ELEMENT, ELASTICITY):
+        return np.ascontiguousarray(coeff, dtype=np.float64).reshape(n, -1)
+    return None
 
 
 def integrate_host_multi(integrators, geoms, coeff_mode=LAPLACE, coeff=None, element_id_base=0, out=None,

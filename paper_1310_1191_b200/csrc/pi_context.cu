@@ -741,9 +741,12 @@ pi_status pi_check(pi_context* ctx, pi_error_info* err) {
   return report_inverted(ctx, gid, got ? g : nullptr, err);
 }
 
-pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
-                            int coeff_mode, const double* coeff, double* out, int64_t chunk_elems,
-                            pi_error_info* err) {
+namespace {
+// pi_integrate_host / pi_integrate_host_load: f, load_out (host) != NULL also
+// stream the load vectors (f per element, or f_const when f == NULL).
+pi_status integrate_host_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
+                              int coeff_mode, const double* coeff, double* out, int64_t chunk_elems,
+                              pi_error_info* err, const double* f, double f_const, double* load_out) {
   if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
   if (!ctx) return set_error(err, PI_E_CONTRACT, "NULL context");
   if (n_elem <= 0) return n_elem == 0 ? PI_OK : set_error(err, PI_E_CONTRACT, "n_elem < 0");
@@ -767,7 +770,9 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
   // per-element coefficient width: the tensor, or (E, nu) for elasticity
   const int cw = coeff_mode == PI_COEFF_PER_ELEMENT ? 16 * ctx->n_eq * ctx->n_eq
                                                     : coeff_mode == PI_COEFF_ELASTICITY ? 2 : 0;
-  const size_t per_elem = sizeof(double) * (kk + 2 * 18 + 2 * cw);
+  const int64_t nsh = ctx->n_shape;
+  const int lw = load_out ? static_cast<int>(nsh) + 1 : 0;  // F and f per element
+  const size_t per_elem = sizeof(double) * (kk + 2 * 18 + 2 * cw + lw);
   if (chunk_elems <= 0) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
@@ -808,6 +813,8 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
     double* d_geom = d_aos + 18 * chunk_elems;
     double* d_caos = d_geom + 18 * chunk_elems;
     double* d_coef = d_caos + cw * chunk_elems;
+    double* d_load = d_coef + cw * chunk_elems;   // [cnt][nsh]
+    double* d_f = d_load + nsh * chunk_elems;      // [cnt]
     PI_CUDA_SETTLE(cudaMemcpyAsync(d_aos, geom_aos + 18 * done, sizeof(double) * 18 * cnt, cudaMemcpyHostToDevice, s),
                    "H2D geometry");
     aos_to_soa_kernel<<<static_cast<unsigned>((18 * cnt + 255) / 256), 256, 0, s>>>(d_aos, d_geom, cnt, 18, cnt);
@@ -820,9 +827,21 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
       cptr = d_coef;
       cld = cnt;
     }
-    pi_status st = pi_integrate(ctx, cnt, element_id_base + done, d_geom, cnt, coeff_mode, cptr, cld, d_out,
-                                PI_OUT_CANONICAL, 0, s, err);
+    pi_status st;
+    if (load_out) {
+      if (f)
+        PI_CUDA_SETTLE(cudaMemcpyAsync(d_f, f + done, sizeof(double) * cnt, cudaMemcpyHostToDevice, s), "H2D f");
+      st = pi_integrate_load(ctx, cnt, element_id_base + done, d_geom, cnt, coeff_mode, cptr, cld, d_out,
+                             PI_OUT_CANONICAL, 0, f ? d_f : nullptr, f_const, d_load, s, err);
+    } else {
+      st = pi_integrate(ctx, cnt, element_id_base + done, d_geom, cnt, coeff_mode, cptr, cld, d_out,
+                        PI_OUT_CANONICAL, 0, s, err);
+    }
     if (st != PI_OK) return settle(st);
+    if (load_out)
+      PI_CUDA_SETTLE(cudaMemcpyAsync(load_out + nsh * done, d_load, sizeof(double) * nsh * cnt,
+                                     cudaMemcpyDeviceToHost, s),
+                     "D2H F");
     PI_CUDA_SETTLE(cudaMemcpyAsync(out + kk * done, d_out, sizeof(double) * kk * cnt, cudaMemcpyDeviceToHost, s),
                    "D2H K");
     done += cnt;
@@ -842,6 +861,26 @@ pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_
   const int64_t gid = static_cast<int64_t>(bad[0]);
   const bool mine = gid >= element_id_base && gid < element_id_base + n_elem;
   return report_inverted(ctx, gid, mine ? geom_aos + 18 * (gid - element_id_base) : nullptr, err);
+}
+
+}  // namespace
+
+pi_status pi_integrate_host(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
+                            int coeff_mode, const double* coeff, double* out, int64_t chunk_elems,
+                            pi_error_info* err) {
+  return integrate_host_impl(ctx, n_elem, element_id_base, geom_aos, coeff_mode, coeff, out, chunk_elems, err,
+                             nullptr, 0.0, nullptr);
+}
+
+pi_status pi_integrate_host_load(pi_context* ctx, int64_t n_elem, int64_t element_id_base, const double* geom_aos,
+                                 int coeff_mode, const double* coeff, const double* f, double f_const, double* out,
+                                 double* load_out, int64_t chunk_elems, pi_error_info* err) {
+  if (!load_out && n_elem > 0) {
+    if (err) std::memset(err, 0, sizeof(*err)), err->element = -1;
+    return set_error(err, PI_E_CONTRACT, "NULL load-vector buffer");
+  }
+  return integrate_host_impl(ctx, n_elem, element_id_base, geom_aos, coeff_mode, coeff, out, chunk_elems, err, f,
+                             f_const, load_out);
 }
 
 pi_status pi_integrate_host_multi(pi_context* const* ctxs, int n_ctx, int64_t n_elem, int64_t element_id_base,

@@ -78,6 +78,31 @@ int main() {
     std::printf("p=%d elasticity vs integrate_optimized: %.3e\n", p, worst);
     if (!(worst <= 1e-12)) ++failures;
   }
+  // stiffness and load vectors in one pass (Context::integrate_with_load):
+  // F = f x column 0 of the c[0][0][0][0] = 1 mass matrix of integrate_generic
+  for (int p : {1, 2, 4}) {
+    const QuadratureRule rule = prism_quadrature(p);
+    const ShapeTable shapes = tabulate_shapes(p, rule);
+    CoefficientTensor lap = CoefficientTensor::zeros(1);
+    for (int d = 1; d <= 3; ++d) lap.set(0, 0, d, d, 1.0);
+    CoefficientTensor mass = CoefficientTensor::zeros(1);
+    mass.set(0, 0, 0, 0, 1.0);
+    std::vector<double> f(mesh.size());
+    for (size_t e = 0; e < mesh.size(); ++e) f[e] = 0.5 + 0.1 * e;
+    prism_b200::Context ctx(shapes, rule);
+    const auto r = ctx.integrate_with_load(mesh, std::span<const CoefficientTensor>(&lap, 1), f);
+    const QuadCoefficients qm = expand_coefficients(mass, rule), ql = expand_coefficients(lap, rule);
+    double worst = 0;
+    for (size_t e = 0; e < mesh.size(); e += 3) {
+      const ElementStiffness m = integrate_generic(mesh[e], qm, shapes, rule);
+      std::vector<double> ref(shapes.n_shape);
+      for (int i = 0; i < shapes.n_shape; ++i) ref[i] = f[e] * m.data[static_cast<size_t>(i) * shapes.n_shape];
+      worst = std::max(worst, rel_frob(ref, r.load[e]));
+      worst = std::max(worst, rel_frob(integrate_generic(mesh[e], ql, shapes, rule).data, r.stiffness[e].data));
+    }
+    std::printf("p=%d integrate_with_load (K and F) vs integrate_generic: %.3e\n", p, worst);
+    if (!(worst <= 1e-12)) ++failures;
+  }
   // several contexts (one per device; here twice the same GPU): bitwise equal
   {
     const int p = 4;

@@ -128,3 +128,24 @@ def test_fused_load_vectors_contract():
         with pytest.raises(pb.ContractViolation):  # load buffer too small
             it.integrate_device(n, geom, torch.empty((n, 18, 18), dtype=torch.float64, device="cuda"), pb.LAPLACE,
                                 load_out=torch.empty((n - 1, 18), dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+def test_host_path_load_vectors(p):
+    """pi_integrate_host_load (the run_batch-style host path, chunked through
+    device memory) equals the device path bit for bit, K and F."""
+    mesh = pb.generate_box_mesh(5, 3, 2, 0.2, seed=23)
+    n = len(mesh)
+    f = np.linspace(0.25, 1.75, n)
+    with pb.Integrator(p) as it:
+        k_h, f_h = it.integrate_host_load(mesh, pb.LAPLACE, f=f, chunk_elems=7)
+        geom = torch.from_numpy(np.ascontiguousarray(mesh.reshape(n, 18).T)).cuda()
+        k_d = torch.empty((n, it.dim, it.dim), dtype=torch.float64, device="cuda")
+        f_d = torch.empty((n, it.n_shape), dtype=torch.float64, device="cuda")
+        it.integrate_device(n, geom, k_d, pb.LAPLACE, load_out=f_d, f=torch.from_numpy(f).cuda())
+        it.check()
+        k_c, f_c = it.integrate_host_load(mesh, pb.LAPLACE, f_const=2.0)
+    assert np.array_equal(k_h, k_d.cpu().numpy()) and np.array_equal(f_h, f_d.cpu().numpy())
+    idx = sample_indices(n, 4)
+    assert rel_frobenius(mass_column_checker(p, mesh[idx], np.full(len(idx), 2.0)), f_c[idx], axis=1).max() <= TOL
+    assert np.array_equal(k_c, k_h)
