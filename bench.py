@@ -24,6 +24,10 @@ Beside the headline the line carries
     reference's integrate_generic, plus a placement check (each sampled element
     re-integrated alone is bitwise equal) and a digest of the sampled matrices
     (equal across N in strong scaling);
+  * `load_vectors`: per p of the step, K alone vs K + load vectors fused into
+    the stiffness kernel vs K + the separate sum-factorised load-vector launch
+    (pi_integrate_load, LOAD_FUSED / LOAD_SEPARATE), the load kernel alone, and
+    F against f x column 0 of the reference's mass matrix;
   * `e2e`: the same step through the host-buffer C-ABI call (pi_integrate_host:
     pinned host geometry in, pinned host K out, all copies timed);
   * `cpu_baseline`: the reference's integrate_generic (oracle/_ref) on the
