@@ -300,10 +300,14 @@ constexpr int load_sf_elems(int ns, int nv) { return ns * nv <= 80 ? 64 : ns * n
 constexpr size_t load_sf_smem(int ns, int nv) {
   return sizeof(double) * (18 * (load_sf_elems(ns, nv) + 1) + load_sf_elems(ns, nv) * ns * nv);
 }
+// P: the degree (compile-time loop bounds: the kernel is instruction-issue
+// bound, ~160 warp instructions per element with runtime bounds at p = 2)
+template <int P>
 __global__ void __launch_bounds__(kLoadSfThreads)
     load_vector_sf_kernel(LaunchArgs args, LoadSfTables tb, const double* f, double f_const) {
-  const int ns = tb.ns, nz = tb.nz, nv = tb.nv, nt = tb.nt, nsh = nt * nv;
-  const int kLoadSfElems = load_sf_elems(ns, nv), kLoadSfPitch = kLoadSfElems + 1;
+  constexpr int nv = P + 1, nz = P + 1, nt = (P + 1) * (P + 2) / 2, nsh = nt * nv;
+  constexpr int ns = P == 1 ? 3 : P == 2 ? 6 : P == 3 ? 12 : P == 4 ? 16 : P == 5 ? 25 : P == 6 ? 33 : 42;
+  constexpr int kLoadSfElems = load_sf_elems(ns, nv), kLoadSfPitch = kLoadSfElems + 1;
   extern __shared__ __align__(16) double sl[];
   double* sX = sl;                          // vertices [18][kLoadSfPitch]
   double* sU = sX + 18 * kLoadSfPitch;      // u [E][ns][nv]
@@ -324,37 +328,39 @@ __global__ void __launch_bounds__(kLoadSfThreads)
     prism_edges(x, d);
     const double fe = f ? f[e0 + el] : f_const;
     const double xi1 = __ldg(tb.tri + s), xi2 = __ldg(tb.tri + ns + s);
-    double u[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double u[nv];
+#pragma unroll
+    for (int a = 0; a < nv; ++a) u[a] = 0.0;
     bool inverted = false;
+#pragma unroll
     for (int z = 0; z < nz; ++z) {
       const double det = jacobian_det(d, xi1, xi2, __ldg(tb.yline + 2 * nv * nz + z));
       inverted |= !(det > 0.0);
       const double dw = det * __ldg(tb.w + z * ns + s) * fe;
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (a < nv) u[a] = fma(__ldg(tb.yline + 2 * (z * nv + a)), dw, u[a]);
+      for (int a = 0; a < nv; ++a) u[a] = fma(__ldg(tb.yline + 2 * (z * nv + a)), dw, u[a]);
     }
     if (inverted) flag_inverted(args.bad, args.element_id_base + e0 + el);
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-      if (a < nv) sU[(el * ns + s) * nv + a] = u[a];
+    for (int a = 0; a < nv; ++a) sU[(el * ns + s) * nv + a] = u[a];
   }
   __syncthreads();
   // thread = (element, t): the nv values F(t, .) share each X_2(t, s) load
   for (int i = tid; i < ne * nt; i += kLoadSfThreads) {
     const int el = i / nt, t = i - el * nt;
     const double* u = sU + el * ns * nv;
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double acc[nv];
+#pragma unroll
+    for (int a = 0; a < nv; ++a) acc[a] = 0.0;
+#pragma unroll 4
     for (int s = 0; s < ns; ++s) {
       const double x2 = __ldg(tb.xplain + (s * 3 + 2) * tb.ntps + t);
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (a < nv) acc[a] = fma(x2, u[s * nv + a], acc[a]);
+      for (int a = 0; a < nv; ++a) acc[a] = fma(x2, u[s * nv + a], acc[a]);
     }
     double* dst = args.out + (e0 + el) * nsh + t * nv;
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-      if (a < nv) dst[a] = acc[a];
+    for (int a = 0; a < nv; ++a) dst[a] = acc[a];
   }
 }
 

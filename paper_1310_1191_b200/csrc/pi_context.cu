@@ -215,8 +215,9 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMalloc"));
   ce = cudaMemset(ctx->d_bad, 0xff, 2 * sizeof(unsigned long long));
   if (ce != cudaSuccess) return fail(cuda_fail(err, ce, "cudaMemset"));
-  cudaFuncSetAttribute(load_vector_sf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       64 * 1024);  // >= load_sf_smem at every p
+  for (auto k : {load_vector_sf_kernel<1>, load_vector_sf_kernel<2>, load_vector_sf_kernel<3>, load_vector_sf_kernel<4>,
+                 load_vector_sf_kernel<5>, load_vector_sf_kernel<6>, load_vector_sf_kernel<7>})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);  // >= load_sf_smem at every p
 
   // The kernels skip the basis' structural zeros (BasisPattern): the table
   // must hold exact zeros there, as tabulate_shapes does.
@@ -651,7 +652,13 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
     const size_t smem = load_sf_smem(ns, ctx->p + 1);
     const int epc = load_sf_elems(ns, ctx->p + 1);
     const unsigned grid = static_cast<unsigned>((n_elem + epc - 1) / epc);
-    load_vector_sf_kernel<<<grid, kLoadSfThreads, smem, s>>>(a, lt, f, f_const);
+    switch (ctx->p) {
+#define PIB_LOAD_CASE(P) \
+  case P: load_vector_sf_kernel<P><<<grid, kLoadSfThreads, smem, s>>>(a, lt, f, f_const); break;
+      PIB_LOAD_CASE(1) PIB_LOAD_CASE(2) PIB_LOAD_CASE(3) PIB_LOAD_CASE(4) PIB_LOAD_CASE(5) PIB_LOAD_CASE(6)
+      PIB_LOAD_CASE(7)
+#undef PIB_LOAD_CASE
+    }
   } else {
     const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);
     load_vector_kernel<<<grid, 32 * kLoadWarps, sizeof(double) * kLoadWarps * ctx->n_q, s>>>(a, t, ctx->n_q,
