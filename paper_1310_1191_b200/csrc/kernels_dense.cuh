@@ -276,6 +276,45 @@ __global__ void __launch_bounds__(32 * kLoadWarps)
   }
 }
 
+// Load vectors at p = 1 (no tensor tables): thread per element, det at the 6
+// rule points, F staged per CTA and stored as one contiguous block.
+constexpr int kLoadP1Threads = 128;
+__global__ void __launch_bounds__(kLoadP1Threads)
+    load_vector_p1_kernel(LaunchArgs args, DenseTables tab, const double* f, double f_const) {
+  constexpr int NQ = 6, NSH = 6;
+  __shared__ double sPhi0[NQ * NSH], sPts[NQ * 3], sW[NQ];
+  __shared__ double sF[kLoadP1Threads * NSH];
+  const int tid = threadIdx.x;
+  if (tid < NQ * NSH) sPhi0[tid] = tab.phi[(tid / NSH) * 4 * NSH + tid % NSH];  // value row phi_0(i, q)
+  if (tid < NQ * 3) sPts[tid] = tab.pts[tid];
+  if (tid < NQ) sW[tid] = tab.w[tid];
+  __syncthreads();
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * kLoadP1Threads, e = first + tid;
+  if (e < args.n_elem) {
+    double x[18], d[21];
+#pragma unroll
+    for (int c = 0; c < 18; ++c) x[c] = args.geom[c * args.geom_ld + e];
+    prism_edges(x, d);
+    const double fe = f ? f[e] : f_const;
+    double F[NSH] = {0, 0, 0, 0, 0, 0};
+    bool inverted = false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double det = jacobian_det(d, sPts[3 * q], sPts[3 * q + 1], sPts[3 * q + 2]);
+      inverted |= !(det > 0.0);
+      const double dw = det * sW[q] * fe;
+#pragma unroll
+      for (int i = 0; i < NSH; ++i) F[i] = fma(dw, sPhi0[q * NSH + i], F[i]);
+    }
+    if (inverted) flag_inverted(args.bad, args.element_id_base + e);
+#pragma unroll
+    for (int i = 0; i < NSH; ++i) sF[tid * NSH + i] = F[i];
+  }
+  __syncthreads();
+  const int n_here = static_cast<int>(min(static_cast<int64_t>(kLoadP1Threads), args.n_elem - first));
+  for (int i = tid; i < n_here * NSH; i += kLoadP1Threads) args.out[first * NSH + i] = sF[i];
+}
+
 // Load vectors through the tensor-product structure (p >= 2 with the
 // sum-factorisation tables): phi_0(t*NV + a, (s, z)) = m_t(s) P_a(z), so
 //     F(t,a) = sum_s X_2(t,s) u(s,a),   u(s,a) = sum_z P_a(z) dw(s,z),

@@ -659,6 +659,9 @@ pi_status pi_load_vectors(pi_context* ctx, int64_t n_elem, int64_t element_id_ba
       PIB_LOAD_CASE(7)
 #undef PIB_LOAD_CASE
     }
+  } else if (ctx->p == 1 && ctx->n_shape == 6 && ctx->n_q == 6) {
+    const unsigned grid = static_cast<unsigned>((n_elem + kLoadP1Threads - 1) / kLoadP1Threads);
+    load_vector_p1_kernel<<<grid, kLoadP1Threads, 0, s>>>(a, t, f, f_const);
   } else {
     const unsigned grid = static_cast<unsigned>((n_elem + kLoadWarps - 1) / kLoadWarps);
     load_vector_kernel<<<grid, 32 * kLoadWarps, sizeof(double) * kLoadWarps * ctx->n_q, s>>>(a, t, ctx->n_q,
