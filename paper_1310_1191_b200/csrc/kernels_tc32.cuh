@@ -1,6 +1,6 @@
 // FP32 variant of the sum-factorised element stiffness on the 5th-generation
 // tensor cores (tcgen05.mma kind::tf32, accumulators in TMEM), p = 3..7,
-// scalar weak forms.  Stated bound 5e-5 (test_kernels.cpp:41-61); measured ~1e-6.
+// scalar weak forms.  Stated bound 5e-5 (test_kernels.cpp:41-61); measured <= 4.2e-7.
 //
 // With the factorisation of kernels_sumfact.cuh,
 //     K[(t,a), j] = sum_(x,s) X_x(t,s) G_x(s,a,j),
@@ -19,11 +19,15 @@
 // point blocks M (FP64, rounded once), per row a the small H_a (FP32), and the
 // G values (3 FMAs + the split each) written straight into the UMMA canonical
 // K-major SWIZZLE_NONE layout (8-row x 16-byte core matrices; 16-byte stores).
-// One thread issues the MMAs (tcgen05.mma) and commits them to mbarriers that
-// free the A buffer (double buffered per (a, m-tile, x)) and publish D; all
-// warps then drain D from TMEM (tcgen05.ld 32x32b: warp w reads lanes
-// 32(w%4)..+31 = rows j) and store K rows (t, a) as coalesced 128-byte
-// segments (lanes = consecutive columns j).
+// Lane 0 of one of the first four warps (round-robin over the rows a) issues
+// a row's MMAs (tcgen05.mma; one thread's stream completes one MMA per ~150
+// cycles whatever its shape, streams of different threads and CTAs overlap)
+// and commits them to mbarriers that free the A buffer (double buffered per
+// (a, m-tile, x)) and publish D; all warps then drain D from TMEM
+// (tcgen05.ld 32x32b: warp w reads lanes 32(w%4)..+31 = rows j) and store K
+// rows (t, a) as coalesced 128-byte segments (lanes = consecutive columns j).
+// Opt-in (PI_VARIANT_TC32): slower than rounding the FP64 DMMA result, the
+// CUDA-core work around the MMAs bounds it.
 #pragma once
 
 #include "kernels_common.cuh"
