@@ -12,9 +12,12 @@
 //    element l;
 //  * warp w (of 3) owns the upper-triangle 3x3 blocks of block rows w and
 //    5-w (7 blocks, 57 accumulators);
-//  * the 6 rule points' physical gradients (18 values) and dw*lam, dw*mu are
-//    computed once per element (2 points per warp) into shared memory, the
+//  * the 6 rule points' physical gradients (18 values) and dw are computed
+//    once per element (2 points per warp) into shared memory, the
 //    structural zeros of the basis skipped at compile time (BasisPattern);
+//  * lam, mu are constant per element, so the lanes accumulate
+//    S_(ie,je) = sum_q dw g_ie(i) g_je(j) (9 FMAs per block and point) and form
+//    K = lam S + mu S^T + mu tr(S) I per block at the end;
 //  * K leaves through shared-memory staging as contiguous coalesced blocks.
 #pragma once
 
@@ -37,10 +40,10 @@ constexpr int kE1Pitch = kE1KK + 2;  // 16-byte multiple: staged elements leave 
 #define PI_E1_ROUND 16
 #endif
 #ifndef PI_E1_MINB
-#define PI_E1_MINB 4
+#define PI_E1_MINB 3
 #endif
 constexpr int kE1Round = PI_E1_ROUND;  // elements staged per output round
-constexpr int kE1NG = 20;            // per point: g_d(i) (18), dw*lam, dw*mu
+constexpr int kE1NG = 19;            // per point: g_d(i) (18), dw
 struct E1Smem {
   static constexpr int GBUF = kE1NQ * kE1NG * 32;
   static constexpr int SBUF = kE1Round * kE1Pitch;
@@ -58,6 +61,10 @@ __device__ __forceinline__ constexpr int e1_brow(int r) {
   return r == 0 ? W : kE1NSH - 1 - W;
 }
 
+// S_(ie,je)(bi, bj) = sum_q dw g_ie(bi) g_je(bj) of the warp's blocks (diagonal
+// blocks: the 6 entries ie <= je of the symmetric S); e1_finish then forms
+// K = lam S + mu S^T + mu tr(S) I per block (lam, mu constant per element):
+// 9 FMAs per block and point instead of the 27-FLOP update.
 template <int W>
 __device__ __forceinline__ void e1_accumulate(const double* __restrict__ sG, int lane, double* acc) {
 #pragma unroll 1
@@ -68,28 +75,53 @@ __device__ __forceinline__ void e1_accumulate(const double* __restrict__ sG, int
     for (int i = 0; i < kE1NSH; ++i)
 #pragma unroll
       for (int d = 0; d < 3; ++d) g[i][d] = gq[(i * 3 + d) * 32];
-    const double lam = gq[18 * 32], mu = gq[19 * 32];
+    const double dw = gq[18 * 32];
     int off = 0;
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
       const int bi = e1_brow<W>(r);
-      double lg[3], mg[3];
+      double wg[3];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        lg[d] = lam * g[bi][d];
-        mg[d] = mu * g[bi][d];
-      }
+      for (int d = 0; d < 3; ++d) wg[d] = dw * g[bi][d];
 #pragma unroll
-      for (int bj = bi; bj < kE1NSH; ++bj) {
-        const double dot = mu * fma(g[bi][0], g[bj][0], fma(g[bi][1], g[bj][1], g[bi][2] * g[bj][2]));
+      for (int bj = bi; bj < kE1NSH; ++bj)
 #pragma unroll
         for (int ie = 0; ie < 3; ++ie)
 #pragma unroll
           for (int je = (bj == bi ? ie : 0); je < 3; ++je) {
-            double v = fma(lg[ie], g[bj][je], fma(mg[je], g[bj][ie], acc[off]));
-            if (ie == je) v += dot;
-            acc[off++] = v;
+            acc[off] = fma(wg[ie], g[bj][je], acc[off]);
+            ++off;
           }
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void e1_finish(double* acc, double lam, double mu) {
+  int off = 0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int bi = e1_brow<W>(r);
+#pragma unroll
+    for (int bj = bi; bj < kE1NSH; ++bj) {
+      if (bj == bi) {  // entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2)
+        const double tr = mu * (acc[off] + acc[off + 3] + acc[off + 5]), lm = lam + mu;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) acc[off + m] = fma(lm, acc[off + m], (m == 0 || m == 3 || m == 5) ? tr : 0.0);
+        off += 6;
+      } else {
+        const double tr = mu * (acc[off] + acc[off + 4] + acc[off + 8]), lm = lam + mu;
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie) {
+          acc[off + ie * 4] = fma(lm, acc[off + ie * 4], tr);
+#pragma unroll
+          for (int je = ie + 1; je < 3; ++je) {
+            const double a = acc[off + ie * 3 + je], b = acc[off + je * 3 + ie];
+            acc[off + ie * 3 + je] = fma(lam, a, mu * b);
+            acc[off + je * 3 + ie] = fma(lam, b, mu * a);
+          }
+        }
+        off += 9;
       }
     }
   }
@@ -175,8 +207,7 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
               if (BP::nz(k + 1, i)) s = fma(ph[(k + 1) * kE1NSH + i], cf[d][k], s);
             gq[(i * 3 + d) * 32] = s * id;
           }
-        gq[18 * 32] = dw * sMat[lane];
-        gq[19 * 32] = dw * sMat[32 + lane];
+        gq[18 * 32] = dw;
       }
       if (inverted && live) flag_inverted(args.bad, args.element_id_base + e);
     }
@@ -184,7 +215,7 @@ __global__ void __launch_bounds__(32 * kE1Warps, PI_E1_MINB) p1_elastic_lane_ker
     double acc[NACC];
 #pragma unroll
     for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
-#define E1_ACC(W) e1_accumulate<W>(sG, lane, acc)
+#define E1_ACC(W) e1_accumulate<W>(sG, lane, acc), e1_finish<W>(acc, sMat[lane], sMat[32 + lane])
     E1_WARP_SWITCH(E1_ACC)
 #undef E1_ACC
     __syncthreads();  // per-point data no longer read: the buffer becomes the output staging
@@ -246,9 +277,11 @@ namespace pib {
 // p = 2 isotropic elasticity (K 54x54): one warp per element, lanes own 3x3
 // blocks.  The 171 upper-triangle shape blocks (i, j >= i) are dealt to the
 // 32 lanes round-robin (5 or 6 blocks, 54 accumulators); per rule point a
-// lane reads the physical gradients g(i), g(j) of its blocks (computed once
-// per element into the warp's shared memory, structural zeros skipped) and
-// updates the 63-flop block of integrate_optimized.  The element matrix is
+// lane reads the physical gradients dw g(i), g(j) of its blocks (computed
+// once per element into the warp's shared memory, structural zeros skipped)
+// and accumulates S_(ie,je) = sum_q dw g_ie(i) g_je(j) (9 FMAs); with lam, mu
+// constant per element the block of integrate_optimized is then
+// lam S + mu S^T + mu tr(S) I (see p3_elastic_mma_kernel).  The element matrix is
 // staged in the warp's shared memory (mirrors included) and leaves with
 // coalesced 16-byte stores.
 constexpr int kE2NQ = 18, kE2NSH = 18, kE2DIM = 54, kE2KK = kE2DIM * kE2DIM, kE2NBLK = 171;
@@ -259,7 +292,8 @@ struct E2Tables {
 
 constexpr int kE2Warps = 4;
 constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
-constexpr int kE2G = kE2NQ * (kE2NSH * 3 + 2);     // per point: g_d(i) (54), dw*lam, dw*mu
+constexpr int kE2GP = kE2NSH * 6;                 // per point: g_d(i) (54), dw g_d(i) (54)
+constexpr int kE2G = kE2NQ * kE2GP;
 constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases the gradients
 constexpr int kE2Phi = kE2NQ * 4 * kE2NSH;          // the shape table, staged per CTA
 constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
@@ -306,7 +340,7 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
       const double det = jacobian_cofactors(d, tb.pts[4 * q], tb.pts[4 * q + 1], tb.pts[4 * q + 2], cf);
       inverted = !(det > 0.0);
       const double id = __drcp_rn(det), dw = det * tb.pts[4 * q + 3];
-      double* gq = sw + q * (kE2NSH * 3 + 2);
+      double* gq = sw + q * kE2GP;
 #pragma unroll
       for (int i = 0; i < kE2NSH; ++i)
 #pragma unroll
@@ -315,14 +349,16 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
 #pragma unroll
           for (int k = 0; k < 3; ++k)
             if (BP::nz(k + 1, i)) s = fma(sPhi[(q * 4 + k + 1) * kE2NSH + i], cf[dd][k], s);
-          gq[i * 3 + dd] = s * id;
+          s *= id;
+          gq[i * 3 + dd] = s;
+          gq[kE2NSH * 3 + i * 3 + dd] = dw * s;
         }
-      gq[kE2NSH * 3] = dw * lam;
-      gq[kE2NSH * 3 + 1] = dw * mu;
     }
     if (__any_sync(0xffffffffu, inverted) && lane == 0) flag_inverted(args.bad, args.element_id_base + e);
     __syncwarp();
-    // ---- accumulate the lane's blocks over the rule points ----
+    // ---- S_(ie,je)(i, j) = sum_q dw g_ie(i) g_je(j) of the lane's blocks ----
+    // (lam, mu are per element: K = lam S + mu S^T + mu tr(S) I per block
+    // afterwards -- 9 FMAs per block and point instead of the 27-FLOP update)
     double acc[kE2BPL][9];
 #pragma unroll
     for (int k = 0; k < kE2BPL; ++k)
@@ -330,26 +366,30 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
       for (int m = 0; m < 9; ++m) acc[k][m] = 0.0;
 #pragma unroll 1
     for (int q = 0; q < kE2NQ; ++q) {
-      const double* gq = sw + q * (kE2NSH * 3 + 2);
-      const double l = gq[kE2NSH * 3], m_ = gq[kE2NSH * 3 + 1];
+      const double* gq = sw + q * kE2GP;
 #pragma unroll
       for (int k = 0; k < kE2BPL; ++k) {
         if (k == kE2BPL - 1 && lane + 32 * k >= kE2NBLK) break;  // lanes 11..31 own 5 blocks
-        const double* gi = gq + bi[k] * 3;
+        const double* gi = gq + kE2NSH * 3 + bi[k] * 3;  // dw g(i)
         const double* gj = gq + bj[k] * 3;
-        const double a0 = gi[0], a1 = gi[1], a2 = gi[2], b0 = gj[0], b1 = gj[1], b2 = gj[2];
-        const double dot = m_ * fma(a0, b0, fma(a1, b1, a2 * b2));
-        const double la[3] = {l * a0, l * a1, l * a2}, ma[3] = {m_ * a0, m_ * a1, m_ * a2};
-        const double bb[3] = {b0, b1, b2};
+        const double a[3] = {gi[0], gi[1], gi[2]}, b[3] = {gj[0], gj[1], gj[2]};
 #pragma unroll
         for (int ie = 0; ie < 3; ++ie)
 #pragma unroll
-          for (int je = 0; je < 3; ++je) {
-            double v = fma(la[ie], bb[je], fma(ma[je], bb[ie], acc[k][ie * 3 + je]));
-            if (ie == je) v += dot;
-            acc[k][ie * 3 + je] = v;
-          }
+          for (int je = 0; je < 3; ++je) acc[k][ie * 3 + je] = fma(a[ie], b[je], acc[k][ie * 3 + je]);
       }
+    }
+#pragma unroll
+    for (int k = 0; k < kE2BPL; ++k) {
+      const double tr = mu * (acc[k][0] + acc[k][4] + acc[k][8]);
+      double kb[9];
+#pragma unroll
+      for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+        for (int je = 0; je < 3; ++je)
+          kb[ie * 3 + je] = fma(lam, acc[k][ie * 3 + je], fma(mu, acc[k][je * 3 + ie], ie == je ? tr : 0.0));
+#pragma unroll
+      for (int m = 0; m < 9; ++m) acc[k][m] = kb[m];
     }
     __syncwarp();  // gradients no longer read: the region becomes the staging of K
     // ---- stage the element matrix (mirrors included), then coalesced stores ----
@@ -527,6 +567,266 @@ __global__ void __launch_bounds__(kE3Threads, 2) p3_elastic_cta_kernel(LaunchArg
         }
     }
     __syncthreads();  // gradients read before the next element overwrites them
+  }
+}
+
+}  // namespace pib
+
+namespace pib {
+
+// ---------------------------------------------------------------------------
+// Isotropic elasticity as one FP64 tensor-core product per element
+// (p3_elastic_mma_kernel, the p = 3 default).  Lam and mu are constant per
+// element, so the block form of integrate_optimized (integrate_ref.cpp:93-130)
+//   K[(i,ie),(j,je)] = sum_q dw [lam g_ie(i) g_je(j) + mu g_je(i) g_ie(j) + mu d_(ie,je) g(i).g(j)]
+// is an epilogue over the nine products
+//   S_(ie,je)(i, j) = sum_q (dw_q g_ie(i, q)) g_je(j, q),
+//   K[(i,ie),(j,je)] = lam S_(ie,je)(i,j) + mu S_(je,ie)(i,j) + mu d_(ie,je) (S_00 + S_11 + S_22)(i,j):
+// a [3 N_sh x N_q] x [N_q x 3 N_sh] product on DMMA m8n8k4 (9 FMAs per block
+// and point instead of the 27-FLOP update, and on the tensor pipe).
+//  * one CTA per element (persistent); threads 0..N_q-1 form the inverse
+//    Jacobian and dw of their rule point, then the CTA writes
+//    B_d(q, i) = g_d(i, q) and A_d(q, i) = dw_q g_d(i, q) to shared memory
+//    ([d][q][i], row pitch = 8 mod 16 doubles: a warp's fragment load is two
+//    conflict-free wavefronts);
+//  * warp w owns PPW (t_i, t_j >= t_i) pairs of 8 x 8 (i, j) tiles and
+//    accumulates the nine S_(ie,je) tiles of each (18 registers per pair);
+//  * the epilogue forms K in registers: a lane holds every (ie, je) of its
+//    (i, j) positions, so row (i, ie) gets 6 consecutive doubles (16-byte
+//    stores); off-diagonal tiles also write the mirror.  The CTA's writes to
+//    one element merge into whole sectors in L2.
+#ifndef PI_EMMA_NW3
+#define PI_EMMA_NW3 5
+#endif
+#ifndef PI_EMMA_GUNROLL
+#define PI_EMMA_GUNROLL 4
+#endif
+constexpr int kEmmaGUnroll = PI_EMMA_GUNROLL;  // gradient-loop unroll (phi loads in flight)
+template <int P>
+struct EMma {
+  static constexpr int NV = P + 1, NTR = (P + 1) * (P + 2) / 2;
+  static constexpr int NSH = NTR * NV;
+  static constexpr int NQ = (P == 1 ? 3 : P == 2 ? 6 : P == 3 ? 12 : P == 4 ? 16 : 25) * (P + 1);
+  static constexpr int NT = (NSH + 7) / 8;                 // 8-wide (i) tiles
+  static constexpr int NSHP = NT * 8 % 16 == 8 ? NT * 8 : NT * 8 + 8;
+  static constexpr int NQP = (NQ + 3) / 4 * 4, KS = NQP / 4;
+  static constexpr int DIM = 3 * NSH;
+  static constexpr int NPAIR = NT * (NT + 1) / 2;
+  static constexpr int NW = P == 3 ? PI_EMMA_NW3 : (NPAIR + 2) / 3;   // warps
+  static constexpr int PPW = (NPAIR + NW - 1) / NW;          // tile pairs per warp
+  static constexpr int NTHREADS = 32 * NW;
+  static constexpr int OFF_A = 0, OFF_B = 3 * NQP * NSHP, OFF_INV = 6 * NQP * NSHP;  // sInv [NQ][10]: inv, dw
+  static constexpr int OFF_X = OFF_INV + NQ * 10;
+  static constexpr int DOUBLES = OFF_X + 18;
+  // staged epilogue: whole tiles only; a warp's 24 x 24 block (row pitch PT)
+  // fits in the dead operands
+  static constexpr int PT = 26;
+#ifdef PI_EMMA_NOPREF
+  static constexpr bool PREFETCH = false;
+#else
+  static constexpr bool PREFETCH = true;
+#endif
+#ifdef PI_EMMA_NOSTAGE
+  static constexpr bool STAGED = false;
+#else
+  static constexpr bool STAGED = NSH % 8 == 0;
+#endif
+  static_assert(!STAGED || NW * 24 * PT <= OFF_INV, "staging fits in the operands");
+  static constexpr size_t BYTES = DOUBLES * sizeof(double);
+  static_assert(NQ <= NTHREADS, "one thread per rule point");
+};
+
+// (t_i, t_j >= t_i) of pair index k in row-major order
+template <int NT>
+__device__ __forceinline__ void emma_pair(int k, int& ti, int& tj) {
+  ti = 0;
+  while (k >= NT - ti) k -= NT - ti++;
+  tj = ti + k;
+}
+
+template <int P>
+__global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(LaunchArgs args, DenseTables tab) {
+  using C = EMma<P>;
+  constexpr int NSH = C::NSH, NQ = C::NQ, NQP = C::NQP, NSHP = C::NSHP, NT = C::NT, PPW = C::PPW, DIM = C::DIM;
+  constexpr int64_t KK = static_cast<int64_t>(DIM) * DIM;
+  constexpr int PT = C::PT;
+  extern __shared__ __align__(16) double em_smem[];
+  double* sA = em_smem + C::OFF_A;
+  double* sB = em_smem + C::OFF_B;
+  double* sInv = em_smem + C::OFF_INV;
+  double* sX = em_smem + C::OFF_X;  // the element's 18 vertex coordinates (prefetched)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // padding rows (q >= NQ) and columns (i >= NSH) stay zero
+  for (int k = tid; k < C::OFF_INV; k += C::NTHREADS) em_smem[k] = 0.0;
+  int ti[PPW], tj[PPW];
+#pragma unroll
+  for (int k = 0; k < PPW; ++k) {
+    const int pk = warp * PPW + k;
+    emma_pair<NT>(pk < C::NPAIR ? pk : C::NPAIR - 1, ti[k], tj[k]);
+  }
+  // whole 8 x 8 tiles, canonical FP64 16-byte aligned output: each tile pair
+  // is staged as a 24 x 24 block of K (over the dead A / B operands) and
+  // leaves as 192-byte row segments, its mirror as the transposed block
+  const bool staged = C::STAGED && args.out_layout == PI_OUT_CANONICAL && !args.out32 &&
+                      (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
+  if (tid < 18 && blockIdx.x < args.n_elem) sX[tid] = args.geom[tid * args.geom_ld + blockIdx.x];
+  __syncthreads();
+  for (int64_t e = blockIdx.x; e < args.n_elem; e += gridDim.x) {
+    double lam, mu;
+    {
+      const double young = args.coeff ? args.coeff[e] : args.cu[0];
+      const double nu = args.coeff ? args.coeff[args.coeff_ld + e] : args.cu[1];
+      if (tid == 0) check_material(args, e, young, nu);
+      lame(young, nu, lam, mu);
+    }
+    // (1) inverse Jacobian and dw per rule point
+    bool inverted = false;
+    if (tid < NQ) {
+      double x[18], d[21];
+#pragma unroll
+      for (int c = 0; c < 18; ++c) x[c] = C::PREFETCH ? sX[c] : args.geom[c * args.geom_ld + e];
+      prism_edges(x, d);
+      const int q = tid;
+      double cf[3][3];
+      const double det = jacobian_cofactors(d, __ldg(tab.pts + 3 * q), __ldg(tab.pts + 3 * q + 1), __ldg(tab.pts + 3 * q + 2), cf);
+      inverted = !(det > 0.0);
+      const double id = __drcp_rn(det);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int dd = 0; dd < 3; ++dd) sInv[q * 10 + k * 3 + dd] = cf[dd][k] * id;  // inv[k][dd]
+      sInv[q * 10 + 9] = det * __ldg(tab.w + q);
+    }
+    // (also: the previous element's staging no longer read)
+    if (__syncthreads_or(inverted) && tid == 0) flag_inverted(args.bad, args.element_id_base + e);
+    // (2) B_d(q, i) = g_d(i, q), A_d(q, i) = dw_q g_d(i, q)
+#pragma unroll kEmmaGUnroll
+    for (int t = tid; t < NQ * NSH; t += C::NTHREADS) {
+      const int q = t / NSH, i = t - q * NSH;
+      const double* ph = tab.phi + q * 4 * NSH + i;
+      const double f1 = __ldg(ph + NSH), f2 = __ldg(ph + 2 * NSH), f3 = __ldg(ph + 3 * NSH);
+      const double* inv = sInv + q * 10;
+      const double dw = inv[9];
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) {
+        const double g = fma(f1, inv[dd], fma(f2, inv[3 + dd], f3 * inv[6 + dd]));
+        sB[(dd * NQP + q) * NSHP + i] = g;
+        sA[(dd * NQP + q) * NSHP + i] = dw * g;
+      }
+    }
+    __syncthreads();
+    // the next element's vertices, in flight during the products
+    // (cp.async: no registers held across the products)
+    const int64_t en = e + gridDim.x;
+    if (C::PREFETCH && tid < 18 && en < args.n_elem) cp_async8(sX + tid, args.geom + tid * args.geom_ld + en);
+    cp_async_commit();
+    // (3) S_(ie,je) tiles of the warp's pairs
+    double acc[PPW][9][2];
+#pragma unroll
+    for (int k = 0; k < PPW; ++k)
+#pragma unroll
+      for (int m = 0; m < 9; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
+    const int fo = (lane & 3) * NSHP + (lane >> 2);  // fragment offset: row q = lane % 4, column lane / 4
+#pragma unroll 2
+    for (int ks = 0; ks < C::KS; ++ks) {
+      const int ko = 4 * ks * NSHP + fo;
+#pragma unroll
+      for (int k = 0; k < PPW; ++k) {
+        double a[3], b[3];
+#pragma unroll
+        for (int dd = 0; dd < 3; ++dd) {
+          a[dd] = sA[dd * NQP * NSHP + ko + 8 * ti[k]];
+          b[dd] = sB[dd * NQP * NSHP + ko + 8 * tj[k]];
+        }
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+          for (int je = 0; je < 3; ++je) dmma_8x8x4(acc[k][ie * 3 + je][0], acc[k][ie * 3 + je][1], a[ie], b[je]);
+      }
+    }
+    cp_async_wait<0>();  // (phase (1) of this element read sX before the barrier after it)
+    if (staged) __syncthreads();  // every warp's products done: A / B become the staging
+    // (4) epilogue: K from S in registers
+    double* sT = em_smem + warp * (24 * PT);  // the warp's 24 x 24 block
+#pragma unroll
+    for (int k = 0; k < PPW; ++k) {
+      if (warp * PPW + k >= C::NPAIR) break;
+      const int il = lane >> 2, jl0 = 2 * (lane & 3);
+      const int i = 8 * ti[k] + il, j0 = 8 * tj[k] + jl0;
+      const bool diag = ti[k] == tj[k];
+      const double tr[2] = {mu * (acc[k][0][0] + acc[k][4][0] + acc[k][8][0]),
+                            mu * (acc[k][0][1] + acc[k][4][1] + acc[k][8][1])};
+      // K row (i, ie), column (j0 + h, je)
+      auto kv = [&](int ie, int je, int h) {
+        return fma(lam, acc[k][ie * 3 + je][h], fma(mu, acc[k][je * 3 + ie][h], ie == je ? tr[h] : 0.0));
+      };
+      const int64_t base = e * KK;
+      if (staged) {
+        // block rows 3 il + ie, columns 3 jl + je; diagonal tiles keep the
+        // upper triangle and mirror it in the block
+#pragma unroll
+        for (int ie = 0; ie < 3; ++ie)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int je = 0; je < 3; ++je) {
+              const int rr = 3 * il + ie, cc = 3 * (jl0 + h) + je;
+              if (diag) {
+                if (rr <= cc) {
+                  const double val = kv(ie, je, h);
+                  sT[rr * PT + cc] = val;
+                  sT[cc * PT + rr] = val;
+                }
+              } else {
+                sT[rr * PT + cc] = kv(ie, je, h);
+              }
+            }
+        __syncwarp();
+        double* rowblk = args.out + base + static_cast<int64_t>(24 * ti[k]) * DIM + 24 * tj[k];
+        // half-warp per row: 24 rows x 12 double2 (lanes 12..15 of each half idle)
+        const int hr = lane >> 4, c2 = lane & 15;
+        if (c2 < 12) {
+#pragma unroll 4
+          for (int rr = hr; rr < 24; rr += 2) {
+            const double2 w = *reinterpret_cast<const double2*>(sT + rr * PT + 2 * c2);
+            *reinterpret_cast<double2*>(rowblk + static_cast<int64_t>(rr) * DIM + 2 * c2) = w;
+          }
+          if (!diag) {  // transposed: row cc of the mirror = column cc of the block
+            double* colblk = args.out + base + static_cast<int64_t>(24 * tj[k]) * DIM + 24 * ti[k];
+#pragma unroll 4
+            for (int cc = hr; cc < 24; cc += 2) {
+              const double2 w = make_double2(sT[(2 * c2) * PT + cc], sT[(2 * c2 + 1) * PT + cc]);
+              *reinterpret_cast<double2*>(colblk + static_cast<int64_t>(cc) * DIM + 2 * c2) = w;
+            }
+          }
+        }
+        __syncwarp();  // block read out before the warp's next pair overwrites it
+      } else if (i < NSH) {
+#pragma unroll
+      for (int ie = 0; ie < 3; ++ie) {
+        const int r = 3 * i + ie;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = j0 + h;
+          if (j >= NSH) continue;
+#pragma unroll
+          for (int je = 0; je < 3; ++je) {
+            const int c = 3 * j + je;
+            if (diag && r > c) continue;  // the lane owning (j, i) writes it
+            const double val = kv(ie, je, h);
+            if (args.out_layout == PI_OUT_SOA) {
+              store_out(args, static_cast<int64_t>(r * DIM + c) * args.ld_out + e, val);
+              if (r != c) store_out(args, static_cast<int64_t>(c * DIM + r) * args.ld_out + e, val);
+            } else {
+              store_out(args, base + static_cast<int64_t>(r) * DIM + c, val);
+              if (r != c) store_out(args, base + static_cast<int64_t>(c) * DIM + r, val);
+            }
+          }
+        }
+      }
+      }
+    }
+    if (!staged) __syncthreads();  // sX written before the next element's phase (1)
   }
 }
 

@@ -282,18 +282,30 @@ pi_status pi_context_create(int device, int p, int n_eq, int n_q, int n_shape, c
       if (ctx->e1tab) ctx->e1tab->pts[4 * q + c] = v;
     }
   if (p == 3 && n_eq == 3) {
+    int per_sm = 0, sms = 0;
+#ifdef PI_E3_CTA  // A/B: the scalar block-update kernel
     cudaFuncSetAttribute(p3_elastic_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(E3Smem::BYTES));
-    int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p3_elastic_cta_kernel, kE3Threads, E3Smem::BYTES);
+#else
+    cudaFuncSetAttribute(p3_elastic_mma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(EMma<3>::BYTES));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p3_elastic_mma_kernel<3>, EMma<3>::NTHREADS, EMma<3>::BYTES);
+#endif
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->e3_ctas = std::max(1, per_sm) * sms;
   }
   if (p == 2 && n_eq == 3) {
+    int per_sm = 0, sms = 0;
+#ifndef PI_E2_MMA
     cudaFuncSetAttribute(p2_elastic_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kE2SmemBytes));
-    int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2_elastic_warp_kernel, 32 * kE2Warps, kE2SmemBytes);
+#else
+    cudaFuncSetAttribute(p3_elastic_mma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(EMma<2>::BYTES));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p3_elastic_mma_kernel<2>, EMma<2>::NTHREADS, EMma<2>::BYTES);
+#endif
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctx->e2_ctas = std::max(1, per_sm) * sms;
   }
@@ -498,10 +510,20 @@ pi_status integrate_impl(pi_context* ctx, int64_t n_elem, int64_t element_id_bas
   if (e3_cta) {
     DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_elem, ctx->e3_ctas));
+#ifdef PI_E3_CTA
     p3_elastic_cta_kernel<<<grid, kE3Threads, E3Smem::BYTES, s>>>(a, t);
+#else
+    p3_elastic_mma_kernel<3><<<grid, EMma<3>::NTHREADS, EMma<3>::BYTES, s>>>(a, t);
+#endif
   } else if (e2_warp) {
+#ifndef PI_E2_MMA
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + kE2Warps - 1) / kE2Warps, ctx->e2_ctas));
     p2_elastic_warp_kernel<<<grid, 32 * kE2Warps, kE2SmemBytes, s>>>(a, *ctx->e2tab);
+#else
+    DenseTables t{ctx->d_phi, ctx->d_pts, ctx->d_w};
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_elem, ctx->e2_ctas));
+    p3_elastic_mma_kernel<2><<<grid, EMma<2>::NTHREADS, EMma<2>::BYTES, s>>>(a, t);
+#endif
   } else if (e1_lane) {
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>((n_elem + 31) / 32, ctx->e1_ctas));
     p1_elastic_lane_kernel<<<grid, 32 * kE1Warps, E1Smem::BYTES, s>>>(a, *ctx->e1tab);
@@ -965,20 +987,28 @@ double pi_flops_executed_per_element(const pi_context* ctx, int coeff_mode) {
   const double per_point = 2.0 * (21 + 16) + 6 + (general ? 200.0 : 48.0);
   const int v = resolve_variant(ctx);
   if (v == PI_VARIANT_DENSE && ctx->n_eq == 3 && p == 3) {
+#ifdef PI_E3_CTA
     // p3_elastic_cta_kernel: inverse per point, 40 gradient triples (9 FMA each),
     // 820 blocks x (3-FMA dot + 9 x 2 FMA + 6 scalings)
     return nq * (2.0 * (21 + 16) + 6 + 2.0 * 40 * 9 + 2.0 * 820 * (3 + 18 + 6));
+#else
+    // p3_elastic_mma_kernel: inverse per point, 40 gradient triples (9 FMA +
+    // 3 dw scalings each); 15 tile pairs x 9 DMMA m8n8k4 (512 FLOPs) per 4
+    // points; the epilogue (about 5 FLOPs per stored upper-triangle entry)
+    return nq * (2.0 * (21 + 16) + 6 + 40 * (2.0 * 9 + 3)) + EMma<3>::NPAIR * 9.0 * 512 * EMma<3>::KS +
+           5.0 * 120 * 121 / 2;
+#endif
   }
   if (v == PI_VARIANT_DENSE && ctx->n_eq == 3 && p == 2) {
-    // p2_elastic_warp_kernel: per point 18 gradient triples (about 2 FMA each),
-    // then 171 blocks x (3-FMA dot + 9 x 2 FMA + 6 scalings)
-    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 18 * 3 * 2 + 2.0 * 171 * (3 + 18 + 6));
+    // p2_elastic_warp_kernel: per point 18 gradient triples (about 2 FMA + 2
+    // scalings each), then 171 blocks x 9 FMA; the epilogue 171 x 9 x 2 FMA + 3
+    return nq * (2.0 * (21 + 16) + 6 + 18 * 3 * (2.0 * 2 + 2) + 2.0 * 171 * 9) + 171 * (2.0 * 18 + 3);
   }
   if (v == PI_VARIANT_DENSE && ctx->n_eq == 3) {
     // p1_elastic_lane_kernel: Jacobian/cofactors, 18 physical gradients
-    // (7 structural non-zeros x 3), then 3 warps x (57 entries x 2 FMA +
-    // 7 block dot products + 12 scaled gradients) per point
-    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 7 * 3 + 2.0 * 3 * (57 * 2 + 7 * 3 + 12));
+    // (7 structural non-zeros x 3), then 3 warps x (57 FMA + 6 dw scalings)
+    // per point; the epilogue about 4 FLOPs per accumulator
+    return nq * (2.0 * (21 + 16) + 6 + 2.0 * 7 * 3 + 3.0 * (57 * 2 + 6)) + 3.0 * 57 * 4;
   }
   if (v == PI_VARIANT_DENSE) {
     // G_l(i) = sum_k phi_k(i) M_kl and K_ij += sum_l G_l(i) phi_l(j) over the
