@@ -606,7 +606,8 @@ template <int P>
 struct EMma {
   static constexpr int NV = P + 1, NTR = (P + 1) * (P + 2) / 2;
   static constexpr int NSH = NTR * NV;
-  static constexpr int NQ = (P == 1 ? 3 : P == 2 ? 6 : P == 3 ? 12 : P == 4 ? 16 : 25) * (P + 1);
+  static constexpr int NS = P == 1 ? 3 : P == 2 ? 6 : P == 3 ? 12 : P == 4 ? 16 : 25, NZ = P + 1;
+  static constexpr int NQ = NS * NZ;  // q = z * NS + s (host_refelem.cpp prism_quadrature)
   static constexpr int NT = (NSH + 7) / 8;                 // 8-wide (i) tiles
   static constexpr int NSHP = NT * 8 % 16 == 8 ? NT * 8 : NT * 8 + 8;
   static constexpr int NQP = (NQ + 3) / 4 * 4, KS = NQP / 4;
@@ -617,15 +618,12 @@ struct EMma {
   static constexpr int NTHREADS = 32 * NW;
   static constexpr int OFF_A = 0, OFF_B = 3 * NQP * NSHP, OFF_INV = 6 * NQP * NSHP;  // sInv [NQ][10]: inv, dw
   static constexpr int OFF_X = OFF_INV + NQ * 10;
-  static constexpr int DOUBLES = OFF_X + 18;
+  static constexpr int OFF_MT = OFF_X + 18;
+  static constexpr int OFF_PZ = OFF_MT + 3 * NTR * NS;
+  static constexpr int DOUBLES = OFF_PZ + 2 * NV * NZ;
   // staged epilogue: whole tiles only; a warp's 24 x 24 block (row pitch PT)
   // fits in the dead operands
   static constexpr int PT = 26;
-#ifdef PI_EMMA_NOPREF
-  static constexpr bool PREFETCH = false;
-#else
-  static constexpr bool PREFETCH = true;
-#endif
 #ifdef PI_EMMA_NOSTAGE
   static constexpr bool STAGED = false;
 #else
@@ -656,8 +654,21 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
   double* sInv = em_smem + C::OFF_INV;
   double* sX = em_smem + C::OFF_X;  // the element's 18 vertex coordinates (prefetched)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* sMt = em_smem + C::OFF_MT;  // m_t(s), dm1_t(s), dm2_t(s): [3][NTR][NS]
+  double* sPz = em_smem + C::OFF_PZ;  // P_a(z), P'_a(z): [2][NV][NZ]
   // padding rows (q >= NQ) and columns (i >= NSH) stay zero
   for (int k = tid; k < C::OFF_INV; k += C::NTHREADS) em_smem[k] = 0.0;
+  // the factors of the tensor basis, read off the shape table: at level z = 0
+  // and a = 0 (P_0 = 1) phi_k((t,0), (0,s)) = m_t(s), dm1_t(s), dm2_t(s); at
+  // t = 0 (m_0 = 1) phi_0 / phi_3((0,a), (z,0)) = P_a(z) / P'_a(z)
+  for (int k = tid; k < 3 * C::NTR * C::NS; k += C::NTHREADS) {
+    const int c = k / (C::NTR * C::NS), t = (k / C::NS) % C::NTR, sp = k % C::NS;
+    sMt[k] = tab.phi[(sp * 4 + c) * NSH + t * C::NV];
+  }
+  for (int k = tid; k < 2 * C::NV * C::NZ; k += C::NTHREADS) {
+    const int c = k / (C::NV * C::NZ), a = (k / C::NZ) % C::NV, z = k % C::NZ;
+    sPz[k] = tab.phi[((z * C::NS) * 4 + (c ? 3 : 0)) * NSH + a];
+  }
   int ti[PPW], tj[PPW];
 #pragma unroll
   for (int k = 0; k < PPW; ++k) {
@@ -669,8 +680,30 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
   // leaves as 192-byte row segments, its mirror as the transposed block
   const bool staged = C::STAGED && args.out_layout == PI_OUT_CANONICAL && !args.out32 &&
                       (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
+  // (1) inverse Jacobian and dw per rule point of element ee, from sX, by the
+  // last NQ threads: for element e+1 this runs between the products and the
+  // epilogue of element e (warp 4 owns the two diagonal tile pairs, the
+  // lightest epilogue), off the critical path of the other warps
+  const int qj = tid - (C::NTHREADS - NQ);
+  auto jacobians = [&](int64_t ee) -> bool {
+    if (qj < 0 || ee >= args.n_elem) return false;
+    double x[18], d[21];
+#pragma unroll
+    for (int c = 0; c < 18; ++c) x[c] = sX[c];
+    prism_edges(x, d);
+    double cf[3][3];
+    const double det = jacobian_cofactors(d, __ldg(tab.pts + 3 * qj), __ldg(tab.pts + 3 * qj + 1), __ldg(tab.pts + 3 * qj + 2), cf);
+    const double id = __drcp_rn(det);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) sInv[qj * 10 + k * 3 + dd] = cf[dd][k] * id;  // inv[k][dd]
+    sInv[qj * 10 + 9] = det * __ldg(tab.w + qj);
+    return !(det > 0.0);
+  };
   if (tid < 18 && blockIdx.x < args.n_elem) sX[tid] = args.geom[tid * args.geom_ld + blockIdx.x];
   __syncthreads();
+  if (__syncthreads_or(jacobians(blockIdx.x)) && tid == 0) flag_inverted(args.bad, args.element_id_base + blockIdx.x);
   for (int64_t e = blockIdx.x; e < args.n_elem; e += gridDim.x) {
     double lam, mu;
     {
@@ -679,46 +712,50 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
       if (tid == 0) check_material(args, e, young, nu);
       lame(young, nu, lam, mu);
     }
-    // (1) inverse Jacobian and dw per rule point
-    bool inverted = false;
-    if (tid < NQ) {
-      double x[18], d[21];
-#pragma unroll
-      for (int c = 0; c < 18; ++c) x[c] = C::PREFETCH ? sX[c] : args.geom[c * args.geom_ld + e];
-      prism_edges(x, d);
-      const int q = tid;
-      double cf[3][3];
-      const double det = jacobian_cofactors(d, __ldg(tab.pts + 3 * q), __ldg(tab.pts + 3 * q + 1), __ldg(tab.pts + 3 * q + 2), cf);
-      inverted = !(det > 0.0);
-      const double id = __drcp_rn(det);
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int dd = 0; dd < 3; ++dd) sInv[q * 10 + k * 3 + dd] = cf[dd][k] * id;  // inv[k][dd]
-      sInv[q * 10 + 9] = det * __ldg(tab.w + q);
-    }
-    // (also: the previous element's staging no longer read)
-    if (__syncthreads_or(inverted) && tid == 0) flag_inverted(args.bad, args.element_id_base + e);
-    // (2) B_d(q, i) = g_d(i, q), A_d(q, i) = dw_q g_d(i, q)
+    // (2) B_d(q, i) = g_d(i, q), A_d(q, i) = dw_q g_d(i, q); with the tensor
+    // basis phi_(t,a) = m_t(xi1, xi2) P_a(xi3) and q = (z, s):
+    //   g_d((t,a), (z,s)) = (inv[0][d] dm1_t(s) + inv[1][d] dm2_t(s)) P_a(z) + inv[2][d] m_t(s) P'_a(z)
+    // one item = (q, t), all a (tables in shared memory, 16-byte stores)
 #pragma unroll kEmmaGUnroll
-    for (int t = tid; t < NQ * NSH; t += C::NTHREADS) {
-      const int q = t / NSH, i = t - q * NSH;
-      const double* ph = tab.phi + q * 4 * NSH + i;
-      const double f1 = __ldg(ph + NSH), f2 = __ldg(ph + 2 * NSH), f3 = __ldg(ph + 3 * NSH);
+    for (int it = tid; it < NQ * C::NTR; it += C::NTHREADS) {
+      const int q = it / C::NTR, t = it - q * C::NTR, z = q / C::NS, sp = q - z * C::NS;
+      const double m = sMt[(0 * C::NTR + t) * C::NS + sp], m1 = sMt[(1 * C::NTR + t) * C::NS + sp],
+                   m2 = sMt[(2 * C::NTR + t) * C::NS + sp];
       const double* inv = sInv + q * 10;
       const double dw = inv[9];
+      double u[3], w[3];
 #pragma unroll
       for (int dd = 0; dd < 3; ++dd) {
-        const double g = fma(f1, inv[dd], fma(f2, inv[3 + dd], f3 * inv[6 + dd]));
-        sB[(dd * NQP + q) * NSHP + i] = g;
-        sA[(dd * NQP + q) * NSHP + i] = dw * g;
+        u[dd] = fma(inv[dd], m1, inv[3 + dd] * m2);
+        w[dd] = inv[6 + dd] * m;
+      }
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) {
+        double g[C::NV];
+#pragma unroll
+        for (int a = 0; a < C::NV; ++a) g[a] = fma(u[dd], sPz[a * C::NZ + z], w[dd] * sPz[(C::NV + a) * C::NZ + z]);
+        double* rb = sB + (dd * NQP + q) * NSHP + t * C::NV;
+        double* ra = sA + (dd * NQP + q) * NSHP + t * C::NV;
+        if constexpr (C::NV % 2 == 0 && NSHP % 2 == 0) {
+#pragma unroll
+          for (int a = 0; a < C::NV; a += 2) {
+            *reinterpret_cast<double2*>(rb + a) = make_double2(g[a], g[a + 1]);
+            *reinterpret_cast<double2*>(ra + a) = make_double2(dw * g[a], dw * g[a + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < C::NV; ++a) {
+            rb[a] = g[a];
+            ra[a] = dw * g[a];
+          }
+        }
       }
     }
     __syncthreads();
     // the next element's vertices, in flight during the products
     // (cp.async: no registers held across the products)
     const int64_t en = e + gridDim.x;
-    if (C::PREFETCH && tid < 18 && en < args.n_elem) cp_async8(sX + tid, args.geom + tid * args.geom_ld + en);
+    if (tid < 18 && en < args.n_elem) cp_async8(sX + tid, args.geom + tid * args.geom_ld + en);
     cp_async_commit();
     // (3) S_(ie,je) tiles of the warp's pairs
     double acc[PPW][9][2];
@@ -744,8 +781,9 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
           for (int je = 0; je < 3; ++je) dmma_8x8x4(acc[k][ie * 3 + je][0], acc[k][ie * 3 + je][1], a[ie], b[je]);
       }
     }
-    cp_async_wait<0>();  // (phase (1) of this element read sX before the barrier after it)
-    if (staged) __syncthreads();  // every warp's products done: A / B become the staging
+    cp_async_wait<0>();
+    __syncthreads();  // every warp's products done: A / B become the staging, sInv is free, sX holds e+1
+    const bool inverted_next = jacobians(en);
     // (4) epilogue: K from S in registers
     double* sT = em_smem + warp * (24 * PT);  // the warp's 24 x 24 block
 #pragma unroll
@@ -826,7 +864,8 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
       }
       }
     }
-    if (!staged) __syncthreads();  // sX written before the next element's phase (1)
+    // element e+1's Jacobians visible; the staging read out before its gradients
+    if (__syncthreads_or(inverted_next) && tid == 0) flag_inverted(args.bad, args.element_id_base + en);
   }
 }
 
