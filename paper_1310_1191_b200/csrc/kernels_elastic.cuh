@@ -292,10 +292,12 @@ struct E2Tables {
 
 constexpr int kE2Warps = 4;
 constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
-constexpr int kE2GP = kE2NSH * 6;                 // per point: g_d(i) (54), dw g_d(i) (54)
+constexpr int kE2GP = kE2NSH * 6 + 1;             // per point: g_d(i) (54), dw g_d(i) (54); odd pitch:
+                                                   // the 18 point lanes write distinct banks
 constexpr int kE2G = kE2NQ * kE2GP;
 constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases the gradients
-constexpr int kE2Phi = kE2NQ * 4 * kE2NSH;          // the shape table, staged per CTA
+constexpr int kE2PhiQ = 4 * kE2NSH + 1;             // staged shape table: odd per-point pitch, so the
+constexpr int kE2Phi = kE2NQ * kE2PhiQ;             // point lanes' reads hit distinct banks
 constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
 
 __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const __grid_constant__ LaunchArgs args,
@@ -306,19 +308,45 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
   double* sw = e2_smem + warp * (kE2WarpDoubles + 2);  // this warp's region (16-byte aligned)
   // lanes read the table at different points: shared memory, not the constant bank
   double* sPhi = e2_smem + (kE2WarpDoubles + 2) * kE2Warps;
-  for (int i = threadIdx.x; i < kE2Phi; i += 32 * kE2Warps) sPhi[i] = tb.phi[i];
+  for (int i = threadIdx.x; i < kE2NQ * 4 * kE2NSH; i += 32 * kE2Warps)
+    sPhi[(i / (4 * kE2NSH)) * kE2PhiQ + i % (4 * kE2NSH)] = tb.phi[i];
   __syncthreads();
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kE2Warps;
-  // the lane's blocks (i, j)
-  int bi[kE2BPL], bj[kE2BPL];
+  // The lane's blocks (i, j): column segments.  Rows fall in three bands of
+  // six (6s .. 6s+5); a lane owns up to six blocks of one column j in one
+  // band, so per point it reads g(j) once (b operand in registers) and
+  // slot k reads dw g(6s + k), which lanes of the same band share
+  // (broadcast): about half the shared-memory wavefronts of a round-robin
+  // deal.  Lanes 0..20 own the 21 full segments (j >= 6s + 5); lanes 21..29
+  // pair the partial diagonal segments of each band (sizes 1 + 5, 2 + 4, 3);
+  // lanes 30, 31 idle.  171 blocks, at most 6 per lane.
+  int bi[kE2BPL], bj[kE2BPL], c0 = 0, c1 = 0;
+  unsigned live = 0u, sel = 0u;  // per slot: stored / reads column c1
+  if (lane < 21) {
+    const int s = lane < 13 ? 0 : lane < 20 ? 1 : 2;
+    const int j = s == 0 ? 5 + lane : s == 1 ? 11 + (lane - 13) : 17;
+    c0 = c1 = j;
 #pragma unroll
-  for (int k = 0; k < kE2BPL; ++k) {
-    // upper-triangle block b = (i, j >= i) in row-major order (padding: b >= 171)
-    int b = lane + 32 * k, i = 0;
-    if (b >= kE2NBLK) b = kE2NBLK - 1;
-    while (b >= kE2NSH - i) b -= kE2NSH - i++;
-    bi[k] = i;
-    bj[k] = i + b;
+    for (int k = 0; k < kE2BPL; ++k) {
+      bi[k] = 6 * s + k;
+      bj[k] = j;
+    }
+    live = 0x3fu;
+  } else {
+    const int m = lane < 30 ? lane - 21 : 8, s = m / 3, r = m % 3;
+    const int ca = 6 * s + r, na = r + 1;                     // column 6s+r: rows 6s .. 6s+r
+    const int cb = 6 * s + 4 - r, nb = r < 2 ? 5 - r : 0;     // column 6s+4-r: rows 6s .. 6s+4-r
+    c0 = nb > 0 ? cb : ca;
+    c1 = ca;
+#pragma unroll
+    for (int k = 0; k < kE2BPL; ++k) {
+      const bool first = k < nb;
+      bi[k] = 6 * s + (first ? k : k - nb);
+      bj[k] = first ? cb : ca;
+      if (!first) sel |= 1u << k;
+      if (lane < 30 && k < nb + na) live |= 1u << k;
+      if (bi[k] > 17) bi[k] = 17;  // dead slots: any valid address
+    }
   }
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kE2Warps + warp; e < args.n_elem; e += nwarps) {
     // ---- geometry, material, then per-point gradients (lane = point) ----
@@ -348,7 +376,7 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
           double s = 0.0;
 #pragma unroll
           for (int k = 0; k < 3; ++k)
-            if (BP::nz(k + 1, i)) s = fma(sPhi[(q * 4 + k + 1) * kE2NSH + i], cf[dd][k], s);
+            if (BP::nz(k + 1, i)) s = fma(sPhi[q * kE2PhiQ + (k + 1) * kE2NSH + i], cf[dd][k], s);
           s *= id;
           gq[i * 3 + dd] = s;
           gq[kE2NSH * 3 + i * 3 + dd] = dw * s;
@@ -367,12 +395,16 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
 #pragma unroll 1
     for (int q = 0; q < kE2NQ; ++q) {
       const double* gq = sw + q * kE2GP;
+      const double b0[3] = {gq[c0 * 3], gq[c0 * 3 + 1], gq[c0 * 3 + 2]};
+      const double b1[3] = {gq[c1 * 3], gq[c1 * 3 + 1], gq[c1 * 3 + 2]};
 #pragma unroll
       for (int k = 0; k < kE2BPL; ++k) {
-        if (k == kE2BPL - 1 && lane + 32 * k >= kE2NBLK) break;  // lanes 11..31 own 5 blocks
         const double* gi = gq + kE2NSH * 3 + bi[k] * 3;  // dw g(i)
-        const double* gj = gq + bj[k] * 3;
-        const double a[3] = {gi[0], gi[1], gi[2]}, b[3] = {gj[0], gj[1], gj[2]};
+        // slots 0..3 always read column c0, slot 5 column c1 (equal to c0 on
+        // single-column lanes); only slot 4 differs between lanes
+        const bool s1 = k == 5 || (k == 4 && ((sel >> 4) & 1u));
+        const double a[3] = {gi[0], gi[1], gi[2]};
+        const double b[3] = {s1 ? b1[0] : b0[0], s1 ? b1[1] : b0[1], s1 ? b1[2] : b0[2]};
 #pragma unroll
         for (int ie = 0; ie < 3; ++ie)
 #pragma unroll
@@ -395,7 +427,7 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
     // ---- stage the element matrix (mirrors included), then coalesced stores ----
 #pragma unroll
     for (int k = 0; k < kE2BPL; ++k) {
-      if (k == kE2BPL - 1 && lane + 32 * k >= kE2NBLK) break;
+      if (!((live >> k) & 1u)) continue;
 #pragma unroll
       for (int ie = 0; ie < 3; ++ie)
 #pragma unroll
