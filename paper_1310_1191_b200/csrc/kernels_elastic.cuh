@@ -296,8 +296,12 @@ constexpr int kE2GP = kE2NSH * 6 + 1;             // per point: g_d(i) (54), dw 
                                                    // the 18 point lanes write distinct banks
 constexpr int kE2G = kE2NQ * kE2GP;
 constexpr int kE2WarpDoubles = kE2KK > kE2G ? kE2KK : kE2G;  // staging aliases the gradients
-constexpr int kE2PhiQ = 4 * kE2NSH + 1;             // staged shape table: odd per-point pitch, so the
-constexpr int kE2Phi = kE2NQ * kE2PhiQ;             // point lanes' reads hit distinct banks
+// per CTA: the factors of the tensor basis phi_(t,a) = m_t(xi1, xi2) P_a(xi3)
+// at the rule points q = (z, s) -- m_t(s), dm1_t(s), dm2_t(s) [3][6][6] and
+// P_a(z), P'_a(z) [2][3][3] -- and the rule [18][4]
+constexpr int kE2NT = 6, kE2NS = 6, kE2NZ = 3, kE2NV = 3;
+constexpr int kE2OffPz = 3 * kE2NT * kE2NS, kE2OffPts = kE2OffPz + 2 * kE2NV * kE2NZ;
+constexpr int kE2Phi = kE2OffPts + 4 * kE2NQ;
 constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
 
 __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const __grid_constant__ LaunchArgs args,
@@ -306,10 +310,26 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
   extern __shared__ __align__(16) double e2_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sw = e2_smem + warp * (kE2WarpDoubles + 2);  // this warp's region (16-byte aligned)
-  // lanes read the table at different points: shared memory, not the constant bank
-  double* sPhi = e2_smem + (kE2WarpDoubles + 2) * kE2Warps;
-  for (int i = threadIdx.x; i < kE2NQ * 4 * kE2NSH; i += 32 * kE2Warps)
-    sPhi[(i / (4 * kE2NSH)) * kE2PhiQ + i % (4 * kE2NSH)] = tb.phi[i];
+  // lanes read the tables at different points: shared memory, not the constant bank
+  double* sMt = e2_smem + (kE2WarpDoubles + 2) * kE2Warps;
+  double* sPz = sMt + kE2OffPz;
+  double* sPts = sMt + kE2OffPts;
+  // read off the shape table (tabulate_shapes order [q][k][dof], q = z*6 + s,
+  // dof = t*3 + a): at z = 0, a = 0 (P_0 = 1) phi_k = m_t(s), dm1_t(s), dm2_t(s);
+  // at t = 0 (m_0 = 1) phi_0 / phi_3 = P_a(z) / P'_a(z)
+  for (int i = threadIdx.x; i < kE2Phi; i += 32 * kE2Warps) {
+    double v;
+    if (i < kE2OffPz) {
+      const int c = i / (kE2NT * kE2NS), t = (i / kE2NS) % kE2NT, sp = i % kE2NS;
+      v = tb.phi[(sp * 4 + c) * kE2NSH + t * kE2NV];
+    } else if (i < kE2OffPts) {
+      const int j = i - kE2OffPz, c = j / (kE2NV * kE2NZ), a = (j / kE2NZ) % kE2NV, z = j % kE2NZ;
+      v = tb.phi[(z * kE2NS * 4 + (c ? 3 : 0)) * kE2NSH + a];
+    } else {
+      v = tb.pts[i - kE2OffPts];
+    }
+    sMt[i] = v;
+  }
   __syncthreads();
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kE2Warps;
   // The lane's blocks (i, j): column segments.  Rows fall in three bands of
@@ -363,24 +383,36 @@ __global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const
     prism_edges(x, d);
     bool inverted = false;
     if (lane < kE2NQ) {
-      const int q = lane;
+      const int q = lane, z = q / kE2NS, sp = q % kE2NS;
       double cf[3][3];
-      const double det = jacobian_cofactors(d, tb.pts[4 * q], tb.pts[4 * q + 1], tb.pts[4 * q + 2], cf);
+      const double det = jacobian_cofactors(d, sPts[4 * q], sPts[4 * q + 1], sPts[4 * q + 2], cf);
       inverted = !(det > 0.0);
-      const double id = __drcp_rn(det), dw = det * tb.pts[4 * q + 3];
+      const double id = __drcp_rn(det), dw = det * sPts[4 * q + 3];
       double* gq = sw + q * kE2GP;
+      double pz[kE2NV], dpz[kE2NV];
 #pragma unroll
-      for (int i = 0; i < kE2NSH; ++i)
+      for (int a = 0; a < kE2NV; ++a) {
+        pz[a] = a == 0 ? 1.0 : sPz[a * kE2NZ + z];
+        dpz[a] = a == 0 ? 0.0 : sPz[(kE2NV + a) * kE2NZ + z];
+      }
+      // g_d((t,a), q) = [(cf[d][0] dm1_t + cf[d][1] dm2_t) P_a + cf[d][2] m_t P'_a] / det
+#pragma unroll
+      for (int t = 0; t < kE2NT; ++t) {
+        const int i0 = t * kE2NV;
+        const double m = sMt[t * kE2NS + sp];
+        const double m1 = BP::nz(1, i0) ? sMt[(kE2NT + t) * kE2NS + sp] : 0.0;
+        const double m2 = BP::nz(2, i0) ? sMt[(2 * kE2NT + t) * kE2NS + sp] : 0.0;
 #pragma unroll
         for (int dd = 0; dd < 3; ++dd) {
-          double s = 0.0;
+          const double u = fma(cf[dd][0], m1, cf[dd][1] * m2), w = cf[dd][2] * m;
 #pragma unroll
-          for (int k = 0; k < 3; ++k)
-            if (BP::nz(k + 1, i)) s = fma(sPhi[q * kE2PhiQ + (k + 1) * kE2NSH + i], cf[dd][k], s);
-          s *= id;
-          gq[i * 3 + dd] = s;
-          gq[kE2NSH * 3 + i * 3 + dd] = dw * s;
+          for (int a = 0; a < kE2NV; ++a) {
+            const double g = (a == 0 ? u : fma(u, pz[a], w * dpz[a])) * id;
+            gq[(i0 + a) * 3 + dd] = g;
+            gq[kE2NSH * 3 + (i0 + a) * 3 + dd] = dw * g;
+          }
         }
+      }
     }
     if (__any_sync(0xffffffffu, inverted) && lane == 0) flag_inverted(args.bad, args.element_id_base + e);
     __syncwarp();
