@@ -42,6 +42,23 @@ def test_lowest_inverted_global_id(p, form):
     assert ei.value.det <= 0.0
 
 
+@pytest.mark.parametrize("p,form", [(1, "laplace"), (2, "laplace"), (3, "laplace"), (4, "cdr"),
+                                    (1, "elasticity"), (2, "elasticity"), (3, "elasticity")])
+def test_inverted_late_in_persistent_loop(p, form):
+    """2048 elements: every CTA of the persistent grids integrates several
+    elements (p3_elastic_mma_kernel forms element e+1's Jacobians inside
+    element e's iteration); inversions far from the first wave are reported,
+    the lowest global id first."""
+    mesh = pb.generate_box_mesh(16, 8, 8, 0.1, seed=p).copy()
+    assert len(mesh) == 2048
+    for e in (1999, 1501):
+        mesh[e, [0, 2]] = mesh[e, [2, 0]]
+    with pytest.raises(pb.InvertedElementError) as ei:
+        run(p, mesh, form, base=10)
+    assert ei.value.element == 1511
+    assert ei.value.det <= 0.0
+
+
 @pytest.mark.parametrize("p", [2, 4])
 def test_inverted_detected_in_f32_variant(p):
     mesh = pb.generate_box_mesh(2, 2, 1, 0.1, seed=1).copy()
