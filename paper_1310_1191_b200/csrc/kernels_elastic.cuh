@@ -666,6 +666,10 @@ namespace pib {
 #define PI_EMMA_GUNROLL 4
 #endif
 constexpr int kEmmaGUnroll = PI_EMMA_GUNROLL;  // gradient-loop unroll (phi loads in flight)
+#ifndef PI_EMMA_KUNROLL
+#define PI_EMMA_KUNROLL 1
+#endif
+constexpr int kEmmaKUnroll = PI_EMMA_KUNROLL;  // product k-loop unroll
 template <int P>
 struct EMma {
   static constexpr int NV = P + 1, NTR = (P + 1) * (P + 2) / 2;
@@ -828,7 +832,7 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
 #pragma unroll
       for (int m = 0; m < 9; ++m) acc[k][m][0] = acc[k][m][1] = 0.0;
     const int fo = (lane & 3) * NSHP + (lane >> 2);  // fragment offset: row q = lane % 4, column lane / 4
-#pragma unroll 2
+#pragma unroll kEmmaKUnroll
     for (int ks = 0; ks < C::KS; ++ks) {
       const int ko = 4 * ks * NSHP + fo;
 #pragma unroll
