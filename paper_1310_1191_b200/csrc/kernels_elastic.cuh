@@ -290,7 +290,13 @@ struct E2Tables {
   double pts[kE2NQ * 4];           // xi1, xi2, xi3, w
 };
 
-constexpr int kE2Warps = 4;
+#ifndef PI_E2_WARPS
+#define PI_E2_WARPS 4
+#endif
+#ifndef PI_E2_MINB
+#define PI_E2_MINB 2
+#endif
+constexpr int kE2Warps = PI_E2_WARPS;
 constexpr int kE2BPL = 6;                          // blocks per lane (ceil(171 / 32))
 constexpr int kE2GP = kE2NSH * 6 + 1;             // per point: g_d(i) (54), dw g_d(i) (54); odd pitch:
                                                    // the 18 point lanes write distinct banks
@@ -304,7 +310,7 @@ constexpr int kE2OffPz = 3 * kE2NT * kE2NS, kE2OffPts = kE2OffPz + 2 * kE2NV * k
 constexpr int kE2Phi = kE2OffPts + 4 * kE2NQ;
 constexpr size_t kE2SmemBytes = sizeof(double) * ((kE2WarpDoubles + 2) * kE2Warps + kE2Phi);
 
-__global__ void __launch_bounds__(32 * kE2Warps, 2) p2_elastic_warp_kernel(const __grid_constant__ LaunchArgs args,
+__global__ void __launch_bounds__(32 * kE2Warps, PI_E2_MINB) p2_elastic_warp_kernel(const __grid_constant__ LaunchArgs args,
                                                                   const __grid_constant__ E2Tables tb) {
   using BP = BasisPattern<2>;
   extern __shared__ __align__(16) double e2_smem[];
