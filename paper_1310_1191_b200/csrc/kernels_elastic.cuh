@@ -654,17 +654,21 @@ namespace pib {
 //   K[(i,ie),(j,je)] = lam S_(ie,je)(i,j) + mu S_(je,ie)(i,j) + mu d_(ie,je) (S_00 + S_11 + S_22)(i,j):
 // a [3 N_sh x N_q] x [N_q x 3 N_sh] product on DMMA m8n8k4 (9 FMAs per block
 // and point instead of the 27-FLOP update, and on the tensor pipe).
-//  * one CTA per element (persistent); threads 0..N_q-1 form the inverse
-//    Jacobian and dw of their rule point, then the CTA writes
-//    B_d(q, i) = g_d(i, q) and A_d(q, i) = dw_q g_d(i, q) to shared memory
-//    ([d][q][i], row pitch = 8 mod 16 doubles: a warp's fragment load is two
-//    conflict-free wavefronts);
+//  * one CTA per element (persistent, two per SM); the last N_q threads
+//    form the inverse Jacobian and dw of their rule point -- for element
+//    e+1 between the products and the epilogue of element e, its vertices
+//    prefetched by cp.async during the products;
+//  * the CTA writes B_d(q, i) = g_d(i, q) and A_d(q, i) = dw_q g_d(i, q) to
+//    shared memory ([d][q][i], row pitch = 8 mod 16 doubles: a warp's
+//    fragment load is two conflict-free wavefronts), the gradients formed
+//    from the factors of the tensor basis phi_(t,a) = m_t P_a;
 //  * warp w owns PPW (t_i, t_j >= t_i) pairs of 8 x 8 (i, j) tiles and
-//    accumulates the nine S_(ie,je) tiles of each (18 registers per pair);
-//  * the epilogue forms K in registers: a lane holds every (ie, je) of its
-//    (i, j) positions, so row (i, ie) gets 6 consecutive doubles (16-byte
-//    stores); off-diagonal tiles also write the mirror.  The CTA's writes to
-//    one element merge into whole sectors in L2.
+//    accumulates the nine S_(ie,je) tiles of each (18 doubles per pair);
+//  * the epilogue forms K in registers (a lane holds every (ie, je) of its
+//    (i, j) positions), stages each tile pair as a 24 x 24 block of K over
+//    the dead operands and writes it as 192-byte row segments, the mirror of
+//    an off-diagonal pair as the transposed block (other layouts / FP32:
+//    scalar stores from registers).
 #ifndef PI_EMMA_NW3
 #define PI_EMMA_NW3 5
 #endif
