@@ -667,8 +667,8 @@ namespace pib {
 //  * the epilogue forms K in registers (a lane holds every (ie, je) of its
 //    (i, j) positions), stages each tile pair as a 24 x 24 block of K over
 //    the dead operands and writes it as 192-byte row segments, the mirror of
-//    an off-diagonal pair as the transposed block (FP32 output: rounded at
-//    those stores; SoA or misaligned outputs: scalar stores from registers).
+//    an off-diagonal pair as the transposed block (other layouts / FP32:
+//    scalar stores from registers).
 #ifndef PI_EMMA_NW3
 #define PI_EMMA_NW3 5
 #endif
@@ -756,11 +756,8 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
   // whole 8 x 8 tiles, canonical FP64 16-byte aligned output: each tile pair
   // is staged as a 24 x 24 block of K (over the dead A / B operands) and
   // leaves as 192-byte row segments, its mirror as the transposed block
-  // (FP32 output: the same blocks, rounded at the 8-byte float2 stores)
-  const bool f32 = args.out32 != nullptr;
-  const bool staged = C::STAGED && args.out_layout == PI_OUT_CANONICAL &&
-                      (f32 ? (reinterpret_cast<uintptr_t>(args.out32) & 7) == 0
-                           : (reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
+  const bool staged = C::STAGED && args.out_layout == PI_OUT_CANONICAL && !args.out32 &&
+                      (reinterpret_cast<uintptr_t>(args.out) & 15) == 0;
   // (1) inverse Jacobian and dw per rule point of element ee, from sX, by the
   // last NQ threads: for element e+1 this runs between the products and the
   // epilogue of element e (warp 4 owns the two diagonal tile pairs, the
@@ -901,27 +898,22 @@ __global__ void __launch_bounds__(EMma<P>::NTHREADS, 2) p3_elastic_mma_kernel(La
               }
             }
         __syncwarp();
-        const int64_t rowoff = base + static_cast<int64_t>(24 * ti[k]) * DIM + 24 * tj[k];
-        const int64_t coloff = base + static_cast<int64_t>(24 * tj[k]) * DIM + 24 * ti[k];
-        // a pair of consecutive K entries: 16-byte (FP64) or 8-byte (FP32) store
-        auto put2 = [&](int64_t idx, double a, double b) {
-          if (f32)
-            *reinterpret_cast<float2*>(args.out32 + idx) = make_float2(static_cast<float>(a), static_cast<float>(b));
-          else
-            *reinterpret_cast<double2*>(args.out + idx) = make_double2(a, b);
-        };
-        // half-warp per row: 24 rows x 12 pairs (lanes 12..15 of each half idle)
+        double* rowblk = args.out + base + static_cast<int64_t>(24 * ti[k]) * DIM + 24 * tj[k];
+        // half-warp per row: 24 rows x 12 double2 (lanes 12..15 of each half idle)
         const int hr = lane >> 4, c2 = lane & 15;
         if (c2 < 12) {
 #pragma unroll 4
           for (int rr = hr; rr < 24; rr += 2) {
             const double2 w = *reinterpret_cast<const double2*>(sT + rr * PT + 2 * c2);
-            put2(rowoff + static_cast<int64_t>(rr) * DIM + 2 * c2, w.x, w.y);
+            *reinterpret_cast<double2*>(rowblk + static_cast<int64_t>(rr) * DIM + 2 * c2) = w;
           }
           if (!diag) {  // transposed: row cc of the mirror = column cc of the block
+            double* colblk = args.out + base + static_cast<int64_t>(24 * tj[k]) * DIM + 24 * ti[k];
 #pragma unroll 4
-            for (int cc = hr; cc < 24; cc += 2)
-              put2(coloff + static_cast<int64_t>(cc) * DIM + 2 * c2, sT[(2 * c2) * PT + cc], sT[(2 * c2 + 1) * PT + cc]);
+            for (int cc = hr; cc < 24; cc += 2) {
+              const double2 w = make_double2(sT[(2 * c2) * PT + cc], sT[(2 * c2 + 1) * PT + cc]);
+              *reinterpret_cast<double2*>(colblk + static_cast<int64_t>(cc) * DIM + 2 * c2) = w;
+            }
           }
         }
         __syncwarp();  // block read out before the warp's next pair overwrites it
